@@ -1,0 +1,151 @@
+/*
+ * plora.h -- C-ABI of libplora, the B200 (sm_100a) packed multi-LoRA hot path.
+ *
+ * This is the drop-in boundary for the reference's packed-LoRA operator API
+ * (`lorasweep.lorapack`, reference pkg/src/lorasweep/lorapack.py:31-42,128-231).
+ * The reference has no FFI of its own (it is pure Python/numpy); its "plugin
+ * interface" is the set of Python functions re-exported at
+ * pkg/src/lorasweep/__init__.py:78-89.  The Python host mirror
+ * `paper_2508_02932_b200.lorapack` keeps those names and binds the entry points
+ * below with ctypes (see INTEGRATION.md for the binding a maintainer would add
+ * to lorasweep itself).
+ *
+ * Conventions
+ *   - Every function returns int status: 0 = ok, non-zero = error; the message
+ *     is available from plora_last_error() (thread-local).  Nothing throws
+ *     across the ABI.
+ *   - All tensor arguments are CALLER-OWNED device buffers (plain pointers);
+ *     no entry point allocates device memory.  Work is enqueued on the
+ *     caller's stream (cudaStream_t passed as void*), stream-ordered and
+ *     re-entrant.
+ *   - Element types: "bf16" = IEEE bfloat16 (uint16 storage), "f32" = float.
+ *   - Shapes are row-major; "[T][d]" means T rows of d contiguous elements.
+ *
+ * Device layouts
+ *   rank blocks : every adapter's rank is zero-padded to rpad64 = 64*nb columns
+ *                 in the bf16 compute shadows (nb = ceil(max_rank/64)), and to
+ *                 rpad16_i = roundup(r_i,16) in fp32 master/grad/moment buffers.
+ *   A_sh  bf16 [n][d][rpad64]  -- adapter down-projection A_i (d x r_i), rank-minor
+ *   Bt_sh bf16 [n][k][rpad64]  -- adapter up-projection  B_i^T (k x r_i), rank-minor
+ *   Hs    bf16 [T][rpad64]     -- alpha_i * X_i A_i  (saved from forward)
+ *   dH    bf16 [T][rpad64]     -- alpha_i * dY_i B_i^T
+ *   gradA f32  region [sum_i d*rpad16_i]: adapter i block [d][rpad16_i] at d*rpad_off[i]
+ *   gradB f32  region [sum_i k*rpad16_i]: adapter i block [k][rpad16_i] at k*rpad_off[i]
+ */
+#ifndef PLORA_H_
+#define PLORA_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define PLORA_API __attribute__((visibility("default")))
+#else
+#define PLORA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLORA_ABI_VERSION 1
+
+/* Device-resident description of one pack (segment index + adapter table).
+ * Built by plora_meta_build on the host, copied to device by the caller. */
+typedef struct plora_pack {
+  int32_t n_adapters;
+  int32_t n_mtiles;        /* entries in d_mtiles */
+  int64_t total_tokens;    /* T = row_offsets[n] */
+  int32_t nb;              /* 64-column rank blocks per adapter in the shadows */
+  int32_t rpad16_total;    /* sum_i rpad16_i */
+  const int32_t* d_mtiles; /* [n_mtiles][4] = {m0, m_len (1..128), adapter, 0} */
+  const int64_t* d_row_off;/* [n+1] token row offsets (reference row_offsets) */
+  const int32_t* d_ranks;  /* [n]   r_i */
+  const int32_t* d_rpad_off;/*[n+1] prefix sums of rpad16_i */
+  const float*   d_alpha;  /* [n]   raw alpha_i (no alpha/r) */
+} plora_pack_t;
+
+/* Library / error plumbing. */
+PLORA_API int plora_abi_version(void);
+PLORA_API const char* plora_last_error(void);
+PLORA_API int plora_device_check(void);   /* 0 iff an sm_100 device is current */
+
+/* K8: segment-index / adapter-metadata builder (host, bit-exact with
+ * lorapack.pack_adapters rank/row offsets, reference lorapack.py:146-150).
+ *   ranks[n] >= 1, tokens[n] >= 0.
+ *   Outputs (caller-allocated host arrays):
+ *     rank_off[n+1], row_off[n+1], rpad_off[n+1]
+ *     mtiles[max_mtiles][4]  (tile list: every tile lies inside one segment)
+ *     token_adapter[T]       (may be NULL)
+ *   *n_mtiles receives the tile count; if it exceeds max_mtiles nothing is
+ *   written to mtiles and status 2 is returned. */
+PLORA_API int plora_meta_build(int32_t n, const int64_t* ranks, const int64_t* tokens,
+                     int64_t* rank_off, int64_t* row_off, int32_t* rpad_off,
+                     int32_t* mtiles, int32_t max_mtiles, int32_t* n_mtiles,
+                     int32_t* token_adapter);
+
+/* Upper bound on the tile count for plora_meta_build. */
+PLORA_API int32_t plora_meta_max_mtiles(int32_t n, const int64_t* tokens);
+
+/* K1 (+K2b): Y[T][N] = A[T][K] * op(W) (+ LoRA expand) (+ residual), bf16 out,
+ * fp32 accumulation in TMEM.  Plain library GEMM entry used by the model for
+ * frozen projections without adapters (lm_head) and by tests.
+ *   w_kmajor = 1: W stored [N][K] (nn.Linear layout, y = x W^T)
+ *   w_kmajor = 0: W stored [K][N] (reference layout,  y = x W)
+ *   pack may be NULL (then M = T rows, single group, no LoRA). */
+PLORA_API int plora_gemm_bf16(void* stream, int64_t M, int64_t N, int64_t K,
+                    const void* A, const void* W, int32_t w_kmajor,
+                    void* Y, int64_t ldy, const void* residual);
+
+/* Packed LoRA linear, forward (reference packed_forward, lorapack.py:183-199):
+ *   Hs = alpha_i * X_i A_i                         (K2a shrink, tcgen05)
+ *   Y  = X op(W) + Hs_i B_i (+ residual)           (K1 GEMM, K2b as extra K-steps)
+ * X bf16 [T][d]; W bf16 [k][d] (w_kmajor=1) or [d][k] (w_kmajor=0);
+ * A_sh, Bt_sh as above; Hs_out bf16 [T][rpad64]; Y bf16 [T][ldy]. */
+PLORA_API int plora_linear_fwd(void* stream, const plora_pack_t* pack,
+                     const void* X, int64_t d, int64_t k,
+                     const void* W, int32_t w_kmajor,
+                     const void* A_sh, const void* Bt_sh,
+                     void* Hs_out, void* Y, int64_t ldy, const void* residual);
+
+/* K1 + K2b only: Y = X op(W) + Hs_i B_i (+ residual) with a caller-provided Hs
+ * (e.g. saved from an earlier shrink, or perturbed by a gradient checker). */
+PLORA_API int plora_linear_expand(void* stream, const plora_pack_t* pack,
+                     const void* X, int64_t d, int64_t k,
+                     const void* W, int32_t w_kmajor, const void* Bt_sh,
+                     const void* Hs, void* Y, int64_t ldy, const void* residual);
+
+/* Packed LoRA linear, backward (reference packed_backward, lorapack.py:202-231):
+ *   dH  = alpha_i dY_i B_i^T                       (Case 2, K4 shrink)
+ *   dB_i^T = Hs_i^T dY_i  -> gradB (f32)           (Case 1, K3 segment reduction)
+ *   dA_i   = X_i^T dH_i   -> gradA (f32)           (Case 3, K5 segment reduction)
+ *   dX  = dY op(W)^T + dH_i A_i^T                  (Case 4, K6 GEMM + extra K-steps)
+ * dX may be NULL (first layer: input gradient not needed).
+ * gradA / gradB are the adapter-major f32 regions described above (written,
+ * not accumulated). dH_ws is a bf16 [T][rpad64] workspace. */
+PLORA_API int plora_linear_bwd(void* stream, const plora_pack_t* pack,
+                     const void* X, int64_t d, int64_t k,
+                     const void* W, int32_t w_kmajor,
+                     const void* A_sh, const void* Bt_sh,
+                     const void* Hs, const void* dY, void* dH_ws,
+                     void* dX, int64_t lddx,
+                     float* gradA, float* gradB);
+
+/* K7: fused per-adapter AdamW (torch.optim.AdamW semantics, decoupled decay)
+ * over fp32 master weights with bf16 shadow write-back.  One call updates
+ * every (layer, target, A|B) region of every adapter.
+ *   chunks: device array [n_chunks][4] int64 =
+ *     {master element offset, shadow element offset, n_rows | rpad16 << 32,
+ *      adapter | shadow_ld << 32}
+ *   hp: device array [n][4] f32 = {lr, weight_decay, unused, unused}
+ *   step: optimizer step count (>= 1) used for bias correction. */
+PLORA_API int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks,
+                float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
+                void* shadow, const float* hp, float beta1, float beta2, float eps,
+                int64_t step);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PLORA_H_ */

@@ -1,0 +1,112 @@
+"""ctypes binding of libplora.so (the C-ABI declared in include/plora.h).
+
+The shared library is built in-tree by ``paper_2508_02932_b200.build``.  There
+is deliberately no fallback: if the library is missing or fails to load, every
+operator raises ``PloraError`` (the product path never silently drops to CPU
+math).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libplora.so"
+
+# Every symbol include/plora.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "plora_abi_version",
+    "plora_last_error",
+    "plora_device_check",
+    "plora_meta_build",
+    "plora_meta_max_mtiles",
+    "plora_gemm_bf16",
+    "plora_linear_fwd",
+    "plora_linear_expand",
+    "plora_linear_bwd",
+    "plora_adamw",
+)
+
+ABI_VERSION = 1
+
+
+class PloraError(RuntimeError):
+    """Raised when a libplora entry point reports failure (or cannot be loaded)."""
+
+
+class PackStruct(ctypes.Structure):
+    """Mirror of ``plora_pack_t`` (include/plora.h)."""
+
+    _fields_ = [
+        ("n_adapters", ctypes.c_int32),
+        ("n_mtiles", ctypes.c_int32),
+        ("total_tokens", ctypes.c_int64),
+        ("nb", ctypes.c_int32),
+        ("rpad16_total", ctypes.c_int32),
+        ("d_mtiles", ctypes.c_void_p),
+        ("d_row_off", ctypes.c_void_p),
+        ("d_ranks", ctypes.c_void_p),
+        ("d_rpad_off", ctypes.c_void_p),
+        ("d_alpha", ctypes.c_void_p),
+    ]
+
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_f32 = ctypes.c_float
+_p64 = ctypes.POINTER(ctypes.c_int64)
+_p32 = ctypes.POINTER(ctypes.c_int32)
+
+_SIGNATURES = {
+    "plora_abi_version": ([], ctypes.c_int),
+    "plora_last_error": ([], ctypes.c_char_p),
+    "plora_device_check": ([], ctypes.c_int),
+    "plora_meta_build": ([_i32, _p64, _p64, _p64, _p64, _p32, _p32, _i32, _p32, _p32], ctypes.c_int),
+    "plora_meta_max_mtiles": ([_i32, _p64], _i32),
+    "plora_gemm_bf16": ([_vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _i64, _vp], ctypes.c_int),
+    "plora_linear_fwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
+                          _vp, _vp, _i64, _vp], ctypes.c_int),
+    "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
+                             _vp, _i64, _vp], ctypes.c_int),
+    "plora_linear_bwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
+                          _vp, _vp, _vp, _vp, _i64, _vp, _vp], ctypes.c_int),
+    "plora_adamw": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _i64],
+                    ctypes.c_int),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the libplora handle; raises PloraError if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise PloraError(
+                f"{LIB_PATH} not built; run `python -m paper_2508_02932_b200.build` "
+                "(or __graft_entry__.build())")
+        try:
+            handle = ctypes.CDLL(str(LIB_PATH))
+        except OSError as exc:  # pragma: no cover - depends on the host
+            raise PloraError(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name, (argtypes, restype) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.argtypes = argtypes
+            fn.restype = restype
+        if handle.plora_abi_version() != ABI_VERSION:
+            raise PloraError("libplora ABI version mismatch; rebuild the extension")
+        _lib = handle
+        return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().plora_last_error().decode(errors="replace")
+        raise PloraError(f"{what} failed ({status}): {msg}")

@@ -1,0 +1,57 @@
+"""Build libplora.so in-tree with nvcc for sm_100a (no JIT cache, travels with the repo)."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libplora.so"
+
+SOURCES = ["plora_abi.cu", "adamw.cu", "meta.cpp"]
+HEADERS = ["sm100.cuh", "gemm_sm100.cuh"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "-Xptxas", "-v",
+    "-shared",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "plora.h", Path(__file__)]
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale():
+        return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
+           *[str(CSRC / s) for s in SOURCES], "-lcuda" if False else "-ldl"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = (res.stdout or "") + (res.stderr or "")
+    (PKG / "build.log").write_text(" ".join(cmd) + "\n" + log)
+    if res.returncode != 0:
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed ({res.returncode}); see {PKG / 'build.log'}")
+    if verbose:
+        sys.stdout.write(log)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

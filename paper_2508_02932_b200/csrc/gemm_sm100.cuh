@@ -1,0 +1,370 @@
+// gemm_sm100.cuh -- the packed-LoRA tensor-core engine for sm_100a.
+//
+// One persistent, warp-specialised tcgen05 kernel template covers every
+// contraction on the packed-LoRA hot path (reference lorapack.py:183-231):
+//
+//   MODE_GEMM   Y[T][N]  = X[T][K] op(W)  (+ Hs_i[T][r] B_i^T  as extra K-steps)  (+ residual)
+//               K1 base projection with K2b fused LoRA expand (forward), and
+//               K6 dX = dY W^T + dH_i A_i^T (backward).  Tiles: 128 token rows of ONE
+//               adapter (segment-index tile list) x BN output columns.
+//   MODE_SHRINK H[T][64nb] = alpha_i X_i[T][K] L_i[K][64nb]
+//               K2a (Hs = alpha X A) and K4 (dH = alpha dY B^T): per-tile adapter operand.
+//   MODE_SEGRED G_i[M][rpad16_i] = sum_{t in segment i} P[t][M]^T Q[t][64nb]
+//               K3 (dB_i^T = Hs_i^T dY_i) and K5 (dA_i = X_i^T dH_i): token-segment
+//               reductions written as fp32 straight into the adapter-major grad region
+//               (deterministic: one CTA owns each output tile, no atomics).
+//
+// Roles (192 threads, 1 CTA/SM): warp 0 = TMA producer, warp 1 = TMEM owner + UMMA
+// issuer (one lane), warps 2..5 = epilogue (TMEM -> registers -> global).
+// Pipelines: smem ring (full/empty mbarriers, TMA complete_tx / tcgen05.commit) and a
+// double-buffered TMEM accumulator (tmem_full/tmem_empty).  All operands are staged by
+// TMA with 128-byte swizzle; UMMA reads them through shared-memory descriptors.
+#pragma once
+#include "sm100.cuh"
+
+namespace plora {
+
+enum GemmMode : int { MODE_GEMM = 0, MODE_SHRINK = 1, MODE_SEGRED = 2 };
+
+struct __align__(64) GemmArgs {
+  CUtensorMap tmA;  // main A operand
+  CUtensorMap tmB;  // main B operand
+  CUtensorMap tmH;  // LoRA-block A operand: Hs or dH, K-major [T][64nb]
+  CUtensorMap tmL;  // LoRA-block B operand: 3D [n][N][64nb], K-major
+  const int32_t* mtiles;    // GEMM/SHRINK tile list [n_groups][4]; nullptr = uniform 128-row tiles
+  const int64_t* row_off;   // SEGRED: token segment offsets [n+1]
+  const int32_t* ranks;     // GEMM with LoRA: r_i
+  const int32_t* rpad_off;  // SEGRED: grad layout prefix sums of rpad16
+  const float* alpha;       // SHRINK: alpha_i
+  void* out;
+  const __nv_bfloat16* residual;  // GEMM: optional, same layout as out
+  int64_t ldo;
+  int32_t M;         // rows (uniform GEMM) or SEGRED output rows (Mdim)
+  int32_t N;         // valid output columns
+  int32_t K;         // reduction length (GEMM/SHRINK)
+  int32_t n_groups;  // row groups
+  int32_t n_ntiles;  // column tiles
+  int32_t mt_per;    // SEGRED: ceil(M/128)
+  int32_t has_lora;
+  int32_t nb;        // 64-column rank blocks
+};
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 192;
+constexpr int kBand = 16;  // row groups per raster band (L2 reuse of the B operand)
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 2;              // 16 KB
+  static constexpr int kBBytes = BN * kBK * 2;               // BN x 64 bf16
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TileInfo {
+  int m0, m_len, adapter, k0, k_len, n0, n_main, n_lora, rank;
+};
+
+template <int BN, int MODE>
+__device__ __forceinline__ TileInfo decode_tile(const GemmArgs& a, int idx) {
+  TileInfo t;
+  int g, nt;
+  if (MODE == MODE_SEGRED) {
+    g = idx / a.n_ntiles;
+    nt = idx - g * a.n_ntiles;
+    t.adapter = g / a.mt_per;
+    t.m0 = (g - t.adapter * a.mt_per) * kBM;
+    t.m_len = min(kBM, a.M - t.m0);
+    const int64_t r0 = a.row_off[t.adapter];
+    t.k0 = static_cast<int>(r0);
+    t.k_len = static_cast<int>(a.row_off[t.adapter + 1] - r0);
+    t.n_lora = 0;
+    t.rank = 0;
+  } else {
+    const int per_band = kBand * a.n_ntiles;
+    const int band = idx / per_band;
+    const int rem = idx - band * per_band;
+    const int g0 = band * kBand;
+    const int bsz = min(kBand, a.n_groups - g0);
+    nt = rem / bsz;
+    g = g0 + (rem - nt * bsz);
+    if (a.mtiles != nullptr) {
+      const int4 mt = reinterpret_cast<const int4*>(a.mtiles)[g];
+      t.m0 = mt.x;
+      t.m_len = mt.y;
+      t.adapter = mt.z;
+    } else {
+      t.m0 = g * kBM;
+      t.m_len = min(kBM, a.M - t.m0);
+      t.adapter = 0;
+    }
+    t.k0 = 0;
+    t.k_len = a.K;
+    if (MODE == MODE_GEMM && a.has_lora) {
+      t.rank = a.ranks[t.adapter];
+      t.n_lora = min((t.rank + 63) / 64, a.nb);
+    } else {
+      t.rank = 0;
+      t.n_lora = 0;
+    }
+  }
+  t.n0 = nt * BN;
+  t.n_main = (t.k_len + kBK - 1) / kBK;
+  return t;
+}
+
+template <int BN, int MODE, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_constant__ GemmArgs args) {
+  using Cfg = GemmCfg<BN>;
+  constexpr bool A_MN = (MODE == MODE_SEGRED);
+  constexpr bool MAIN_B_MN = (MODE == MODE_GEMM) ? B_MN : true;
+  constexpr int S = Cfg::kStages;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int total = args.n_groups * args.n_ntiles;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&args.tmA);
+    tma_prefetch(&args.tmB);
+    if (MODE == MODE_GEMM && args.has_lora) {
+      tma_prefetch(&args.tmH);
+      tma_prefetch(&args.tmL);
+    }
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+        const TileInfo t = decode_tile<BN, MODE>(args, idx);
+        const int nblk = t.n_main + t.n_lora;
+        for (int b = 0; b < nblk; ++b) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * Cfg::kStageBytes;
+          uint8_t* sB = sA + Cfg::kABytes;
+          mbar_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          if (b < t.n_main) {
+            const int kc = t.k0 + b * kBK;
+            if (A_MN) {
+              tma_load_2d(sA, &args.tmA, &full_bar[stage], t.m0, kc);
+              tma_load_2d(sA + 8192, &args.tmA, &full_bar[stage], t.m0 + 64, kc);
+            } else {
+              tma_load_2d(sA, &args.tmA, &full_bar[stage], kc, t.m0);
+            }
+            if (MODE == MODE_SHRINK) {
+              tma_load_3d(sB, &args.tmB, &full_bar[stage], t.n0, kc, t.adapter);
+            } else if (MAIN_B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sB + j * 8192, &args.tmB, &full_bar[stage], t.n0 + 64 * j, kc);
+            } else {
+              tma_load_2d(sB, &args.tmB, &full_bar[stage], kc, t.n0);
+            }
+          } else {
+            const int lb = b - t.n_main;
+            tma_load_2d(sA, &args.tmH, &full_bar[stage], lb * 64, t.m0);
+            tma_load_3d(sB, &args.tmL, &full_bar[stage], lb * 64, t.n0, t.adapter);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ UMMA issuer
+    constexpr uint32_t idesc_main = idesc_bf16(kBM, BN, A_MN, MAIN_B_MN);
+    constexpr uint32_t idesc_lora = idesc_bf16(kBM, BN, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      const TileInfo t = decode_tile<BN, MODE>(args, idx);
+      const int nblk = t.n_main + t.n_lora;
+      if (nblk == 0) continue;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int b = 0; b < nblk; ++b) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        uint8_t* sA = smem + stage * Cfg::kStageBytes;
+        uint8_t* sB = sA + Cfg::kABytes;
+        const bool lora = b >= t.n_main;
+        if (MODE == MODE_SEGRED) {
+          // Token rows past the segment end belong to the next adapter: zero them in
+          // both operands before the tensor core reads the stage.
+          const int valid = t.k_len - b * kBK;
+          if (valid < kBK) {
+            const int nrows = kBK - valid;
+            const int per = nrows * 8;  // 16-byte chunks per sub-tile
+            for (int i = lane; i < 3 * per; i += 32) {
+              const int sub = i / per;
+              const int rem = i - sub * per;
+              uint8_t* base = (sub < 2) ? (sA + sub * 8192) : sB;
+              reinterpret_cast<uint4*>(base + (valid + rem / 8) * 128)[rem % 8] = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+          }
+        }
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA);
+          const uint32_t b0 = smem_u32(sB);
+          int ksteps = 4;
+          if (lora) ksteps = min(4, (t.rank - (b - t.n_main) * 64 + 15) / 16);
+          for (int ks = 0; ks < ksteps; ++ks) {
+            uint64_t ad, bd;
+            if (!lora && A_MN) ad = smem_desc_sw128(a0 + ks * 2048, 8192, 1024);
+            else               ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
+            if (!lora && MAIN_B_MN) bd = smem_desc_sw128(b0 + ks * 2048, 8192, 1024);
+            else                    bd = smem_desc_sw128(b0 + ks * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, lora ? idesc_lora : idesc_main, (b > 0 || ks > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      const TileInfo t = decode_tile<BN, MODE>(args, idx);
+      const int nblk = t.n_main + t.n_lora;
+      if (MODE == MODE_SEGRED) {
+        const int ld = args.rpad_off[t.adapter + 1] - args.rpad_off[t.adapter];
+        float* g = reinterpret_cast<float*>(args.out) +
+                   static_cast<int64_t>(args.M) * args.rpad_off[t.adapter];
+        const bool row_ok = row < t.m_len;
+        float* grow = g + static_cast<int64_t>(t.m0 + row) * ld;
+        if (nblk == 0) {
+          if (row_ok)
+            for (int c = t.n0; c < min(t.n0 + BN, ld); c += 4)
+              *reinterpret_cast<float4*>(grow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          continue;
+        }
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tb + c * 32, r);
+          tmem_ld_wait();
+          const int col0 = t.n0 + c * 32;
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              if (col0 + j < ld)
+                *reinterpret_cast<float4*>(grow + col0 + j) =
+                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          }
+        }
+      } else {
+        if (nblk == 0) continue;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+        const float scale = (MODE == MODE_SHRINK) ? args.alpha[t.adapter] : 1.0f;
+        const bool row_ok = row < t.m_len;
+        const int64_t orow = static_cast<int64_t>(t.m0 + row) * args.ldo;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow;
+        const __nv_bfloat16* res = (MODE == MODE_GEMM && args.residual) ? args.residual + orow : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tb + c * 32, r);
+          tmem_ld_wait();
+          const int col0 = t.n0 + c * 32;
+          if (row_ok && col0 < args.N) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * scale;
+            if (col0 + 32 <= args.N) {
+              if (res) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint4 rv = *reinterpret_cast<const uint4*>(res + col0 + q * 8);
+                  const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                  for (int h = 0; h < 4; ++h) {
+                    const float2 f = __bfloat1622float2(rh[h]);
+                    v[q * 8 + 2 * h] += f.x;
+                    v[q * 8 + 2 * h + 1] += f.y;
+                  }
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint4 w;
+                w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+                w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+                w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+                w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+                *reinterpret_cast<uint4*>(o + col0 + q * 8) = w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (col0 + j < args.N) {
+                  float x = v[j];
+                  if (res) x += __bfloat162float(res[col0 + j]);
+                  o[col0 + j] = __float2bfloat16_rn(x);
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace plora

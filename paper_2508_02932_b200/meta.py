@@ -1,0 +1,139 @@
+"""Segment-index / adapter-metadata builder (K8) -- host side of the pack.
+
+Mirrors the offset bookkeeping of the reference ``pack_adapters``
+(pkg/src/lorasweep/lorapack.py:146-150): ``rank_offsets`` and ``row_offsets``
+are exact integer prefix sums, returned as tuples of Python ints so they compare
+equal (bit-exactly) to the reference's.  The arithmetic runs in the C++ builder
+behind the C-ABI (``plora_meta_build``, csrc/meta.cpp); this module only
+marshals arrays and uploads the device copy the kernels read.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass
+class PackMeta:
+    """Host + device description of one pack (n adapters over T packed tokens)."""
+
+    ranks: tuple[int, ...]
+    tokens: tuple[int, ...]
+    alphas: tuple[float, ...]
+    rank_offsets: tuple[int, ...]
+    row_offsets: tuple[int, ...]
+    rpad_off: np.ndarray          # int32 [n+1], prefix sums of roundup(r_i, 16)
+    mtiles: np.ndarray            # int32 [n_mtiles, 4]
+    token_adapter: np.ndarray     # int32 [T]
+    nb: int                       # 64-column rank blocks in the bf16 shadows
+    device: object = None
+    _dev: dict = field(default_factory=dict, repr=False)
+    _struct: _lib.PackStruct | None = field(default=None, repr=False)
+
+    @property
+    def n_adapters(self) -> int:
+        return len(self.ranks)
+
+    @property
+    def total_tokens(self) -> int:
+        return self.row_offsets[-1]
+
+    @property
+    def rpad64(self) -> int:
+        return 64 * self.nb
+
+    @property
+    def rpad16(self) -> np.ndarray:
+        return np.diff(self.rpad_off).astype(np.int64)
+
+    @property
+    def rpad16_total(self) -> int:
+        return int(self.rpad_off[-1])
+
+    def to(self, device) -> "PackMeta":
+        """Upload the device copy (int tables + alphas) and build the plora_pack_t."""
+        import torch
+
+        device = torch.device(device)
+        if self.device is not None and torch.device(self.device) == device and self._struct is not None:
+            return self
+        dev = {
+            "mtiles": torch.from_numpy(np.ascontiguousarray(self.mtiles, dtype=np.int32)).to(device),
+            "row_off": torch.tensor(self.row_offsets, dtype=torch.int64, device=device),
+            "ranks": torch.tensor(self.ranks, dtype=torch.int32, device=device),
+            "rpad_off": torch.from_numpy(self.rpad_off.astype(np.int32)).to(device),
+            "alpha": torch.tensor(self.alphas, dtype=torch.float32, device=device),
+        }
+        s = _lib.PackStruct()
+        s.n_adapters = self.n_adapters
+        s.n_mtiles = int(self.mtiles.shape[0])
+        s.total_tokens = self.total_tokens
+        s.nb = self.nb
+        s.rpad16_total = self.rpad16_total
+        s.d_mtiles = dev["mtiles"].data_ptr() if s.n_mtiles else None
+        s.d_row_off = dev["row_off"].data_ptr()
+        s.d_ranks = dev["ranks"].data_ptr()
+        s.d_rpad_off = dev["rpad_off"].data_ptr()
+        s.d_alpha = dev["alpha"].data_ptr()
+        self._dev = dev
+        self._struct = s
+        self.device = device
+        return self
+
+    @property
+    def struct(self) -> _lib.PackStruct:
+        if self._struct is None:
+            raise _lib.PloraError("PackMeta not uploaded; call .to(device) first")
+        return self._struct
+
+    def dev(self, name: str):
+        return self._dev[name]
+
+
+def build_meta(ranks: Sequence[int], tokens: Sequence[int], alphas: Sequence[float],
+               nb: int | None = None) -> PackMeta:
+    """Build the pack metadata through ``plora_meta_build`` (C++ K8)."""
+    n = len(ranks)
+    if n == 0:
+        raise ValueError("nothing to pack")
+    if len(tokens) != n or len(alphas) != n:
+        raise ValueError(f"{n} adapters but {len(tokens)} inputs")
+    L = _lib.lib()
+    r = np.ascontiguousarray(ranks, dtype=np.int64)
+    t = np.ascontiguousarray(tokens, dtype=np.int64)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    p32 = ctypes.POINTER(ctypes.c_int32)
+    max_tiles = int(L.plora_meta_max_mtiles(n, t.ctypes.data_as(p64)))
+    rank_off = np.zeros(n + 1, dtype=np.int64)
+    row_off = np.zeros(n + 1, dtype=np.int64)
+    rpad_off = np.zeros(n + 1, dtype=np.int32)
+    mtiles = np.zeros((max(max_tiles, 1), 4), dtype=np.int32)
+    n_tiles = ctypes.c_int32(0)
+    total = int(t.sum()) if n else 0
+    tok_ad = np.zeros(max(total, 1), dtype=np.int32)
+    rc = L.plora_meta_build(n, r.ctypes.data_as(p64), t.ctypes.data_as(p64),
+                            rank_off.ctypes.data_as(p64), row_off.ctypes.data_as(p64),
+                            rpad_off.ctypes.data_as(p32), mtiles.ctypes.data_as(p32),
+                            max(max_tiles, 1), ctypes.byref(n_tiles), tok_ad.ctypes.data_as(p32))
+    if rc != 0:
+        raise ValueError(L.plora_last_error().decode())
+    max_rank = int(r.max())
+    need_nb = (max_rank + 63) // 64
+    nb = need_nb if nb is None else max(int(nb), need_nb)
+    return PackMeta(
+        ranks=tuple(int(x) for x in r),
+        tokens=tuple(int(x) for x in t),
+        alphas=tuple(float(a) for a in alphas),
+        rank_offsets=tuple(int(x) for x in rank_off),
+        row_offsets=tuple(int(x) for x in row_off),
+        rpad_off=rpad_off,
+        mtiles=mtiles[: n_tiles.value].copy(),
+        token_adapter=tok_ad[:total].copy(),
+        nb=nb,
+    )

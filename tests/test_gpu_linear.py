@@ -1,0 +1,121 @@
+"""Packed LoRA linear at bench-like sizes through the torch-tensor ABI (ops.*),
+checked against a torch fp32 reference of the same bf16 operands, plus
+size-independent properties (linearity in alpha, packing invariance)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2508_02932_b200 import ops
+from paper_2508_02932_b200.meta import build_meta
+
+pytestmark = pytest.mark.gpu
+
+bf = torch.bfloat16
+
+
+def make(ranks, tokens, d, k, seed=0, kmajor=True):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    n = len(ranks)
+    alphas = [float(r) * m for r, m in zip(ranks, [0.25, 1.0, 2.0, 4.0] * 8)]
+    meta = build_meta(ranks, tokens, alphas).to("cuda")
+    T = meta.total_tokens
+    R64 = meta.rpad64
+    x = torch.randn(T, d, device="cuda", generator=g).to(bf)
+    w = (torch.randn(k, d, device="cuda", generator=g) * 0.02 if kmajor else
+         torch.randn(d, k, device="cuda", generator=g) * 0.02).to(bf)
+    a_sh = torch.zeros(n, d, R64, device="cuda", dtype=bf)
+    bt_sh = torch.zeros(n, k, R64, device="cuda", dtype=bf)
+    for i, r in enumerate(ranks):
+        a_sh[i, :, :r] = ((torch.rand(d, r, device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(bf)
+        bt_sh[i, :, :r] = (torch.randn(k, r, device="cuda", generator=g) * 0.02).to(bf)
+    dy = (torch.randn(T, k, device="cuda", generator=g) * 0.1).to(bf)
+    return meta, x, w, a_sh, bt_sh, dy
+
+
+def reference(meta, x, w, kmajor, a_sh, bt_sh, dy):
+    W = w.float().t() if kmajor else w.float()
+    y = x.float() @ W
+    dx = dy.float() @ W.t()
+    dA, dB, hs_all = [], [], []
+    for i in range(meta.n_adapters):
+        s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+        r = meta.ranks[i]
+        al = meta.alphas[i]
+        A = a_sh[i, :, :r].float()
+        B = bt_sh[i, :, :r].float().t()
+        xi, dyi = x[s:e].float(), dy[s:e].float()
+        hs = (al * (xi @ A)).to(bf).float()          # the kernel stores Hs in bf16
+        y[s:e] += hs @ B
+        dh = (al * (dyi @ B.t())).to(bf).float()     # and dH in bf16
+        dx[s:e] += dh @ A.t()
+        dB.append(dyi.t() @ hs)                      # dB^T [k][r]
+        dA.append(xi.t() @ dh)                       # dA [d][r]
+        hs_all.append(hs)
+    return y, dx, dA, dB
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("kmajor", [True, False])
+@pytest.mark.parametrize("d,k", [(4096, 4096), (4096, 1024), (1024, 3072)])
+def test_packed_linear_vs_torch(kmajor, d, k):
+    ranks = [8, 16, 32, 64]
+    tokens = [1024, 512, 1024, 2048]
+    meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, k, seed=d + k, kmajor=kmajor)
+    y, hs = ops.linear_fwd(meta, x, w, kmajor, a_sh, bt_sh)
+    R16 = meta.rpad16_total
+    ga = torch.empty(d * R16, device="cuda")
+    gb = torch.empty(k * R16, device="cuda")
+    dx = ops.linear_bwd(meta, x, w, kmajor, a_sh, bt_sh, hs, dy, ga, gb)
+    ry, rdx, rdA, rdB = reference(meta, x, w, kmajor, a_sh, bt_sh, dy)
+    assert rel(y, ry) < 1e-2
+    assert rel(dx, rdx) < 1e-2
+    for i, r in enumerate(ranks):
+        rp = int(meta.rpad_off[i + 1] - meta.rpad_off[i])
+        blk_a = ga[d * int(meta.rpad_off[i]): d * int(meta.rpad_off[i + 1])].view(d, rp)
+        blk_b = gb[k * int(meta.rpad_off[i]): k * int(meta.rpad_off[i + 1])].view(k, rp)
+        assert rel(blk_a[:, :r], rdA[i]) < 5e-3, ("dA", i)
+        assert rel(blk_b[:, :r], rdB[i]) < 5e-3, ("dB", i)
+        assert not torch.any(blk_a[:, r:]) and not torch.any(blk_b[:, r:])   # padding stays zero
+
+
+def test_packing_invariance():
+    """Adapter i's outputs/grads in a pack equal running it alone."""
+    d, k = 1024, 2048
+    ranks, tokens = [8, 64, 16], [256, 384, 128]
+    meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, k, seed=5)
+    y, hs = ops.linear_fwd(meta, x, w, True, a_sh, bt_sh)
+    ga = torch.empty(d * meta.rpad16_total, device="cuda")
+    gb = torch.empty(k * meta.rpad16_total, device="cuda")
+    dx = ops.linear_bwd(meta, x, w, True, a_sh, bt_sh, hs, dy, ga, gb)
+    for i in range(3):
+        s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+        solo = build_meta([ranks[i]], [tokens[i]], [meta.alphas[i]], nb=meta.nb).to("cuda")
+        ys, hss = ops.linear_fwd(solo, x[s:e].contiguous(), w, True, a_sh[i:i + 1].contiguous(),
+                                 bt_sh[i:i + 1].contiguous())
+        gas = torch.empty(d * solo.rpad16_total, device="cuda")
+        gbs = torch.empty(k * solo.rpad16_total, device="cuda")
+        dxs = ops.linear_bwd(solo, x[s:e].contiguous(), w, True, a_sh[i:i + 1].contiguous(),
+                             bt_sh[i:i + 1].contiguous(), hss, dy[s:e].contiguous(), gas, gbs)
+        assert torch.equal(ys, y[s:e])          # same tiles, same math: bit-identical
+        assert torch.equal(dxs, dx[s:e])
+        off = int(meta.rpad_off[i])
+        rp = solo.rpad16_total
+        assert torch.equal(gas, ga[d * off: d * (off + rp)])
+        assert torch.equal(gbs, gb[k * off: k * (off + rp)])
+
+
+def test_deterministic_grads():
+    meta, x, w, a_sh, bt_sh, dy = make([8, 16, 32, 64], [1024, 1024, 2048, 1024], 2048, 2048, seed=9)
+    outs = []
+    for _ in range(2):
+        y, hs = ops.linear_fwd(meta, x, w, True, a_sh, bt_sh)
+        ga = torch.empty(2048 * meta.rpad16_total, device="cuda")
+        gb = torch.empty(2048 * meta.rpad16_total, device="cuda")
+        dx = ops.linear_bwd(meta, x, w, True, a_sh, bt_sh, hs, dy, ga, gb)
+        outs.append((y, dx, ga, gb))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
