@@ -108,6 +108,16 @@ PLORA_API int plora_linear_fwd(void* stream, const plora_pack_t* pack,
                      const void* A_sh, const void* Bt_sh,
                      void* Hs_out, void* Y, int64_t ldy, const void* residual);
 
+/* K2a / K4 alone: out[T][rpad64] = alpha_i * P_i[T_i][K] * L_i[K][rpad64],
+ * L stored [n][K][rpad64] (A_sh for the forward shrink, Bt_sh for dH). */
+PLORA_API int plora_lora_shrink(void* stream, const plora_pack_t* pack, int64_t K,
+                     const void* P, const void* L_sh, void* out);
+
+/* K3 / K5 alone: G_i[Mdim][rpad16_i] = P_i^T Q_i over segment i's tokens, fp32,
+ * written into the adapter-major region G (P bf16 [T][Mdim], Q bf16 [T][rpad64]). */
+PLORA_API int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t Mdim,
+                     const void* P, const void* Q, float* G);
+
 /* K1 + K2b only: Y = X op(W) + Hs_i B_i (+ residual) with a caller-provided Hs
  * (e.g. saved from an earlier shrink, or perturbed by a gradient checker). */
 PLORA_API int plora_linear_expand(void* stream, const plora_pack_t* pack,
@@ -120,7 +130,9 @@ PLORA_API int plora_linear_expand(void* stream, const plora_pack_t* pack,
  *   dB_i^T = Hs_i^T dY_i  -> gradB (f32)           (Case 1, K3 segment reduction)
  *   dA_i   = X_i^T dH_i   -> gradA (f32)           (Case 3, K5 segment reduction)
  *   dX  = dY op(W)^T + dH_i A_i^T                  (Case 4, K6 GEMM + extra K-steps)
- * dX may be NULL (first layer: input gradient not needed).
+ * dX may be NULL (first layer: input gradient not needed).  dX_residual (may be
+ * NULL, same layout as dX) is added in the dX epilogue, so the input gradients of
+ * several linears that share an input (q/k/v, gate/up) accumulate without a pass.
  * gradA / gradB are the adapter-major f32 regions described above (written,
  * not accumulated). dH_ws is a bf16 [T][rpad64] workspace. */
 PLORA_API int plora_linear_bwd(void* stream, const plora_pack_t* pack,
@@ -128,7 +140,7 @@ PLORA_API int plora_linear_bwd(void* stream, const plora_pack_t* pack,
                      const void* W, int32_t w_kmajor,
                      const void* A_sh, const void* Bt_sh,
                      const void* Hs, const void* dY, void* dH_ws,
-                     void* dX, int64_t lddx,
+                     void* dX, int64_t lddx, const void* dX_residual,
                      float* gradA, float* gradB);
 
 /* K7: fused per-adapter AdamW (torch.optim.AdamW semantics, decoupled decay)

@@ -23,6 +23,8 @@ EXPORTS = (
     "plora_meta_max_mtiles",
     "plora_gemm_bf16",
     "plora_linear_fwd",
+    "plora_lora_shrink",
+    "plora_lora_segred",
     "plora_linear_expand",
     "plora_linear_bwd",
     "plora_adamw",
@@ -71,10 +73,12 @@ _SIGNATURES = {
     "plora_gemm_bf16": ([_vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_fwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                           _vp, _vp, _i64, _vp], ctypes.c_int),
+    "plora_lora_shrink": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp], ctypes.c_int),
+    "plora_lora_segred": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                              _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_bwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
-                          _vp, _vp, _vp, _vp, _i64, _vp, _vp], ctypes.c_int),
+                          _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_adamw": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _i64],
                     ctypes.c_int),
 }

@@ -270,6 +270,21 @@ int plora_linear_fwd(void* stream, const plora_pack_t* pack, const void* X, int6
                   residual);
 }
 
+int plora_lora_shrink(void* stream, const plora_pack_t* pack, int64_t K, const void* P,
+                      const void* L_sh, void* out) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  return run_shrink(static_cast<cudaStream_t>(stream), pack, K, P, L_sh, out);
+}
+
+int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t Mdim, const void* P,
+                      const void* Q, float* G) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (!G) return fail("segred: output region is NULL");
+  return run_segred(static_cast<cudaStream_t>(stream), pack, Mdim, P, Q, G);
+}
+
 int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int64_t k,
                         const void* W, int32_t w_kmajor, const void* Bt_sh, const void* Hs, void* Y,
                         int64_t ldy, const void* residual) {
@@ -282,7 +297,7 @@ int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, i
 int plora_linear_bwd(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int64_t k,
                      const void* W, int32_t w_kmajor, const void* A_sh, const void* Bt_sh,
                      const void* Hs, const void* dY, void* dH_ws, void* dX, int64_t lddx,
-                     float* gradA, float* gradB) {
+                     const void* dX_residual, float* gradA, float* gradB) {
   int rc;
   if ((rc = check_pack(pack))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -296,7 +311,7 @@ int plora_linear_bwd(void* stream, const plora_pack_t* pack, const void* X, int6
   //   nn.Linear W [k][d] is MN-major for this product; reference W [d][k] is K-major.
   if (dX)
     return run_gemm(st, pack, pack->total_tokens, d, k, dY, W, w_kmajor ? 0 : 1, dH_ws, A_sh, dX,
-                    lddx, nullptr);
+                    lddx, dX_residual);
   return 0;
 }
 

@@ -322,7 +322,7 @@ def _rel_err(analytic: np.ndarray, numeric: np.ndarray) -> float:
     return float(np.max(np.abs(analytic - numeric) / scale))
 
 
-def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: float = 0.5,
+def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: float = 4.0,
                tolerance: float = GRAD_CHECK_TOLERANCE) -> GradCheckReport:
     """Finite-difference check of the GPU gradients (reference lorapack.py:279-340).
 

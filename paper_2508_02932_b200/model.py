@@ -1,0 +1,347 @@
+"""Packed multi-LoRA training step on a frozen Llama/Qwen2-style decoder.
+
+Every one of the 7 LoRA targets per layer (q, k, v, o, gate, up, down)
+is a packed LoRA linear executed by libplora (K2a shrink -> K1 tcgen05 GEMM with the
+K2b expand fused as extra K-steps; backward K4 -> K3/K5 segment reductions -> K6
+dX GEMM with the LoRA term as extra K-steps).  Token segments are adapter-major:
+adapter i owns b_i whole sequences of length s, so attention never crosses
+adapters.  The frozen lm_head runs on the same tcgen05 GEMM engine.  The loss is
+sum_i mean_{tokens of i} CE, so every adapter's gradient equals its solo-training
+gradient.
+
+Off the hot path (plain torch / fused helpers in ``elementwise``): embedding
+gather, RMSNorm, RoPE, SwiGLU, attention (torch SDPA), cross-entropy.
+
+The backward is written out explicitly (no autograd tape) so that exactly the
+tensors listed in ``_LayerSave`` are kept: per layer the residual input, the
+post-attention residual, q/k/v (inside the attention graph), the attention output,
+gate/up projections and the 7 bf16 Hs tiles; normed inputs and SwiGLU output are
+recomputed.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+import torch.nn.functional as F
+
+from . import elementwise as ew
+from . import ops
+from .adapters import AdapterBank, Target
+from .meta import PackMeta, build_meta
+
+bf16 = torch.bfloat16
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    d: int
+    n_layers: int
+    ffn: int
+    n_heads: int
+    n_kv: int
+    vocab: int
+    tied: bool = False
+    rope_theta: float = 500000.0
+    norm_eps: float = 1e-5
+    qkv_bias: bool = False
+    rope_llama3: bool = False
+
+    @property
+    def head_dim(self) -> int:
+        return self.d // self.n_heads
+
+    def targets(self) -> list[Target]:
+        hd = self.head_dim
+        return [Target("q", self.d, self.n_heads * hd), Target("k", self.d, self.n_kv * hd),
+                Target("v", self.d, self.n_kv * hd), Target("o", self.n_heads * hd, self.d),
+                Target("gate", self.d, self.ffn), Target("up", self.d, self.ffn),
+                Target("down", self.ffn, self.d)]
+
+    def base_linear_params(self) -> int:
+        """Sum of h_in*h_out over the targeted projections plus the lm_head."""
+        per_layer = sum(t.h_in * t.h_out for t in self.targets())
+        return self.n_layers * per_layer + self.d * self.vocab
+
+    def base_flops_per_token(self) -> float:
+        """Base-GEMM roofline FLOPs/token: 4 * (sum h_in*h_out + d*V) (fwd X W + bwd dY W^T;
+        the base is frozen so there is no dW).  SURVEY.md section 8(d)."""
+        return 4.0 * self.base_linear_params()
+
+    def lora_flops_per_token_per_rank(self) -> float:
+        """6 * sum(h_in + h_out) * L: matches lora_flop (costmodel.py:168-178)."""
+        return 6.0 * self.n_layers * sum(t.h_in + t.h_out for t in self.targets())
+
+
+PRESETS = {
+    # C1: tiny 2-layer transformer, runs on the CPU reference
+    "tiny": ModelConfig("tiny-d256", d=256, n_layers=2, ffn=1024, n_heads=4, n_kv=4, vocab=1024,
+                        rope_theta=10000.0),
+    # C2: Qwen2.5-3B (tied embeddings, q/k/v bias)
+    "qwen2.5-3b": ModelConfig("Qwen2.5-3B", d=2048, n_layers=36, ffn=11008, n_heads=16, n_kv=2,
+                              vocab=151936, tied=True, rope_theta=1000000.0, norm_eps=1e-6, qkv_bias=True),
+    # C3: Llama-3.1-8B
+    "llama-3.1-8b": ModelConfig("Llama-3.1-8B", d=4096, n_layers=32, ffn=14336, n_heads=32, n_kv=8,
+                                vocab=128256, rope_theta=500000.0, norm_eps=1e-5, rope_llama3=True),
+    # C4: Qwen2.5-32B
+    "qwen2.5-32b": ModelConfig("Qwen2.5-32B", d=5120, n_layers=64, ffn=27648, n_heads=40, n_kv=8,
+                               vocab=152064, rope_theta=1000000.0, norm_eps=1e-6, qkv_bias=True),
+}
+
+
+@dataclass(frozen=True)
+class AdapterSpec:
+    """One packed adapter: rank, raw alpha, sequences per step, learning rate."""
+    rank: int
+    alpha: float
+    batch: int
+    lr: float
+    weight_decay: float = 0.0
+
+
+# The bench configurations of SURVEY.md section 8(d).
+def bench_adapters(cfg_name: str) -> tuple[list[AdapterSpec], int]:
+    mults = [0.25, 1.0, 2.0, 4.0]
+    lrs = [2e-5, 5e-5, 1e-4, 2e-4, 4e-4]
+    if cfg_name == "tiny":
+        ranks, batch, s = [8, 16, 32, 64], [1, 2, 1, 2], 128
+    elif cfg_name == "qwen2.5-3b":
+        ranks, batch, s = [8, 16, 32, 64] * 2, [1, 2, 4, 1, 2, 4, 1, 2], 1024
+    elif cfg_name == "llama-3.1-8b":
+        ranks = [8, 16, 32, 64] * 4
+        batch, s = [1, 1, 2, 4, 2, 1, 4, 1, 1, 2, 1, 4, 4, 2, 1, 1], 1024
+    elif cfg_name == "qwen2.5-32b":
+        ranks, batch, s = [8, 16, 32, 64] * 8, [1] * 32, 1024
+    else:
+        raise KeyError(cfg_name)
+    specs = [AdapterSpec(rank=r, alpha=r * mults[i % 4], batch=b, lr=lrs[i % 5])
+             for i, (r, b) in enumerate(zip(ranks, batch))]
+    return specs, s
+
+
+class BaseWeights:
+    """Frozen bf16 base model (random init N(0, 0.02^2), seed 0; norms = 1).
+    Projection weights use the nn.Linear layout [h_out][h_in] (K-major operand)."""
+
+    def __init__(self, cfg: ModelConfig, device="cuda", seed: int = 0, std: float = 0.02):
+        self.cfg = cfg
+        g = torch.Generator(device=device).manual_seed(seed)
+
+        def rnd(*shape):
+            return (torch.randn(*shape, generator=g, device=device) * std).to(bf16)
+
+        self.embed = rnd(cfg.vocab, cfg.d)
+        self.layers = []
+        for _ in range(cfg.n_layers):
+            lw = {t.name: rnd(t.h_out, t.h_in) for t in cfg.targets()}
+            lw["attn_norm"] = torch.ones(cfg.d, device=device, dtype=bf16)
+            lw["mlp_norm"] = torch.ones(cfg.d, device=device, dtype=bf16)
+            if cfg.qkv_bias:
+                for t in ("q", "k", "v"):
+                    lw[t + "_bias"] = rnd(lw[t].shape[0])
+            self.layers.append(lw)
+        self.final_norm = torch.ones(cfg.d, device=device, dtype=bf16)
+        self.lm_head = self.embed if cfg.tied else rnd(cfg.vocab, cfg.d)
+
+    def nbytes(self) -> int:
+        n = self.embed.numel() + self.final_norm.numel()
+        if not self.cfg.tied:
+            n += self.lm_head.numel()
+        for lw in self.layers:
+            n += sum(v.numel() for v in lw.values())
+        return 2 * n
+
+
+def rope_tables(cfg: ModelConfig, seq_len: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    hd = cfg.head_dim
+    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.float64, device=device) / hd))
+    if cfg.rope_llama3:  # Llama-3.1 frequency scaling (factor 8, low/high freq 1/4, orig ctx 8192)
+        factor, lo, hi, orig = 8.0, 1.0, 4.0, 8192.0
+        wavelen = 2 * math.pi / inv
+        smooth = (orig / wavelen - lo) / (hi - lo)
+        scaled = torch.where(wavelen > orig / lo, inv / factor, inv)
+        mid = (wavelen <= orig / lo) & (wavelen >= orig / hi)
+        scaled = torch.where(mid, (1 - smooth) * inv / factor + smooth * inv, scaled)
+        inv = scaled
+    pos = torch.arange(seq_len, dtype=torch.float64, device=device)
+    ang = torch.outer(pos, inv)
+    return ang.cos().float().contiguous(), ang.sin().float().contiguous()
+
+
+@dataclass
+class _LayerSave:
+    h_in: torch.Tensor
+    rstd1: torch.Tensor
+    h_mid: torch.Tensor
+    rstd2: torch.Tensor
+    attn_graph: tuple
+    attn_out: torch.Tensor
+    g: torch.Tensor
+    u: torch.Tensor
+    hs: dict = field(default_factory=dict)
+
+
+class PackedLoraTrainer:
+    """One packed job: n heterogeneous adapters trained concurrently on one frozen base."""
+
+    def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
+                 base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
+                 a_scale: float | None = None, b_std: float = 0.02):
+        self.cfg = cfg
+        self.specs = list(specs)
+        self.s = seq_len
+        self.device = torch.device(device)
+        tokens = [sp.batch * seq_len for sp in specs]
+        self.meta: PackMeta = build_meta([sp.rank for sp in specs], tokens, [sp.alpha for sp in specs]).to(
+            self.device)
+        self.T = self.meta.total_tokens
+        self.base = base or BaseWeights(cfg, self.device)
+        self.bank = AdapterBank(self.meta, cfg.n_layers, cfg.targets(), [sp.lr for sp in specs],
+                                [sp.weight_decay for sp in specs], device=self.device, seeds=adapter_seeds,
+                                a_scale=a_scale, b_std=b_std)
+        self.cos, self.sin = rope_tables(cfg, seq_len, self.device)
+        self.ce_chunk = ce_chunk
+        # per-token adapter id and the CE weight 1/n_i (labels exist for s-1 tokens per sequence)
+        ta = torch.from_numpy(self.meta.token_adapter.astype("int64")).to(self.device)
+        n_lab = torch.tensor([max(sp.batch * (seq_len - 1), 1) for sp in specs], dtype=torch.float32,
+                             device=self.device)
+        pos = torch.arange(self.T, device=self.device) % seq_len
+        self.token_adapter = ta
+        self.has_label = pos != seq_len - 1
+        self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
+        self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
+
+    # ------------------------------------------------------------------ helpers
+    def _lin_fwd(self, layer: int, tname: str, x: torch.Tensor, w: torch.Tensor, residual=None):
+        a_sh = self.bank.shadow_of(layer, tname, "A")
+        bt_sh = self.bank.shadow_of(layer, tname, "B")
+        y, hs = ops.linear_fwd(self.meta, x, w, True, a_sh, bt_sh, residual=residual)
+        return y, hs
+
+    def _lin_bwd(self, layer: int, tname: str, x, w, hs, dy, need_dx=True, dx_residual=None, dx_out=None):
+        bank = self.bank
+        return ops.linear_bwd(self.meta, x, w, True, bank.shadow_of(layer, tname, "A"),
+                              bank.shadow_of(layer, tname, "B"), hs, dy,
+                              bank.region_flat(bank.G, layer, tname, "A"),
+                              bank.region_flat(bank.G, layer, tname, "B"),
+                              dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
+
+    # ------------------------------------------------------------------ forward
+    def _layer_fwd(self, layer: int, h: torch.Tensor) -> tuple[torch.Tensor, _LayerSave]:
+        cfg, lw = self.cfg, self.base.layers[layer]
+        T, hd, H, KV = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv
+        B = T // self.s
+        x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
+        q, hs_q = self._lin_fwd(layer, "q", x1, lw["q"])
+        k, hs_k = self._lin_fwd(layer, "k", x1, lw["k"])
+        v, hs_v = self._lin_fwd(layer, "v", x1, lw["v"])
+        if cfg.qkv_bias:
+            q += lw["q_bias"]
+            k += lw["k_bias"]
+            v += lw["v_bias"]
+        q = ew.rope_fwd(q.view(B, self.s, H, hd), self.cos, self.sin)
+        k = ew.rope_fwd(k.view(B, self.s, KV, hd), self.cos, self.sin)
+        qg = q.transpose(1, 2).detach().requires_grad_()
+        kg = k.transpose(1, 2).detach().requires_grad_()
+        vg = v.view(B, self.s, KV, hd).transpose(1, 2).detach().requires_grad_()
+        with torch.enable_grad():
+            og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
+        attn = og.detach().transpose(1, 2).reshape(T, H * hd)
+        h_mid, hs_o = self._lin_fwd(layer, "o", attn, lw["o"], residual=h)
+        x2, rstd2 = ew.rmsnorm_fwd(h_mid, lw["mlp_norm"], cfg.norm_eps)
+        g, hs_g = self._lin_fwd(layer, "gate", x2, lw["gate"])
+        u, hs_u = self._lin_fwd(layer, "up", x2, lw["up"])
+        act = ew.swiglu_fwd(g, u)
+        h_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"], residual=h_mid)
+        save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
+                          attn_out=attn, g=g, u=u,
+                          hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d})
+        return h_out, save
+
+    # ------------------------------------------------------------------ backward
+    def _layer_bwd(self, layer: int, sv: _LayerSave, dh: torch.Tensor, need_dx: bool) -> torch.Tensor:
+        cfg, lw = self.cfg, self.base.layers[layer]
+        T, hd, H, KV = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv
+        B = T // self.s
+        # MLP: h_out = h_mid + down(swiglu(gate(x2), up(x2)))
+        act = ew.swiglu_fwd(sv.g, sv.u)
+        d_act = self._lin_bwd(layer, "down", act, lw["down"], sv.hs["down"], dh)
+        del act
+        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u)
+        del d_act
+        x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
+        dx2 = self._lin_bwd(layer, "up", x2, lw["up"], sv.hs["up"], du)
+        dx2 = self._lin_bwd(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
+        del dg, du
+        d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh)
+        del dx2, x2
+        # attention: h_mid = h_in + o(attn(rope(q(x1)), rope(k(x1)), v(x1)))
+        d_attn = self._lin_bwd(layer, "o", sv.attn_out, lw["o"], sv.hs["o"], d_mid)
+        qg, kg, vg, og = sv.attn_graph
+        dog = d_attn.view(B, self.s, H, hd).transpose(1, 2)
+        dq, dk, dv = torch.autograd.grad(og, (qg, kg, vg), dog)
+        del d_attn, dog
+        dq = ew.rope_bwd(dq.transpose(1, 2), self.cos, self.sin).reshape(T, H * hd)
+        dk = ew.rope_bwd(dk.transpose(1, 2), self.cos, self.sin).reshape(T, KV * hd)
+        dv = dv.transpose(1, 2).reshape(T, KV * hd)
+        x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
+        dx1 = self._lin_bwd(layer, "v", x1, lw["v"], sv.hs["v"], dv)
+        dx1 = self._lin_bwd(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1)
+        dx1 = self._lin_bwd(layer, "q", x1, lw["q"], sv.hs["q"], dq, dx_residual=dx1, dx_out=dx1)
+        del dq, dk, dv, x1
+        if not need_dx:
+            return None
+        return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid)
+
+    # ------------------------------------------------------------------ loss head
+    def _head(self, h: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
+        """Final norm + lm_head + per-adapter-mean CE, chunked over tokens; returns d h.
+        Accumulates per-adapter losses into self.losses."""
+        cfg = self.cfg
+        xf, rstd = ew.rmsnorm_fwd(h, self.base.final_norm, cfg.norm_eps)
+        dxf = torch.empty_like(xf)
+        labels = torch.roll(tokens, -1)
+        self.losses.zero_()
+        for c0 in range(0, self.T, self.ce_chunk):
+            c1 = min(self.T, c0 + self.ce_chunk)
+            logits = ops.gemm(xf[c0:c1], self.base.lm_head, True)
+            ew.cross_entropy_fwd_bwd(logits, labels[c0:c1], self.ce_weight[c0:c1],
+                                     self.token_adapter[c0:c1], self.losses)
+            ops.gemm(logits, self.base.lm_head, False, out=dxf[c0:c1])   # dX = dlogits @ W_lm
+            del logits
+        return ew.rmsnorm_bwd(dxf, h, rstd, self.base.final_norm)
+
+    # ------------------------------------------------------------------ step
+    def forward_backward(self, tokens: torch.Tensor) -> torch.Tensor:
+        """Full packed forward + backward; fills bank.G; returns per-adapter losses (device)."""
+        h = self.base.embed[tokens]
+        saves = []
+        for layer in range(self.cfg.n_layers):
+            h, sv = self._layer_fwd(layer, h)
+            saves.append(sv)
+        dh = self._head(h, tokens)
+        del h
+        for layer in reversed(range(self.cfg.n_layers)):
+            sv = saves.pop()
+            dh = self._layer_bwd(layer, sv, dh, need_dx=layer > 0)
+            del sv
+        return self.losses
+
+    def step(self, tokens: torch.Tensor) -> torch.Tensor:
+        """forward + backward + fused per-adapter AdamW (K7)."""
+        losses = self.forward_backward(tokens)
+        self.bank.adamw_step()
+        return losses
+
+    # ------------------------------------------------------------------ data
+    def synthetic_tokens(self, seed_base: int = 1000) -> torch.Tensor:
+        """tokens ~ U{0..V-1}, seed 1000+i per adapter."""
+        parts = []
+        for i, sp in enumerate(self.specs):
+            g = torch.Generator(device="cpu").manual_seed(seed_base + i)
+            parts.append(torch.randint(0, self.cfg.vocab, (sp.batch * self.s,), generator=g))
+        return torch.cat(parts)

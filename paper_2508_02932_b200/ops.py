@@ -20,6 +20,59 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+class KernelTimer:
+    """Per-kernel-class CUDA-event timing inside a timed region (bench.py roofline).
+
+    While active, packed linears are issued as their component launches
+    (shrink / segment reductions / GEMM) with events recorded on the launching
+    stream around each, together with that launch's ALGORITHMIC flops and bytes."""
+
+    def __init__(self):
+        self.records: list[tuple[str, torch.cuda.Event, torch.cuda.Event, float, float]] = []
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0):
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.records.append((kind, e0, e1, flops, nbytes))
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for kind, e0, e1, fl, nb in self.records:
+            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+            d["launches"] += 1
+            d["ms"] += e0.elapsed_time(e1)
+            d["flops"] += fl
+            d["bytes"] += nb
+        return out
+
+
+_TIMER: KernelTimer | None = None
+_LAUNCHES = [0]
+
+
+def set_timer(t: KernelTimer | None) -> None:
+    global _TIMER
+    _TIMER = t
+
+
+def launch_count() -> int:
+    """Number of libplora kernel launches issued by this process so far."""
+    return _LAUNCHES[0]
+
+
+def _lora_work(meta: PackMeta) -> tuple[int, int]:
+    """(sum_i T_i r_i, R = sum_i r_i) for the algorithmic-work formulas."""
+    if not hasattr(meta, "_work"):
+        meta._work = (sum(t * r for t, r in zip(meta.tokens, meta.ranks)), sum(meta.ranks))
+    return meta._work
+
+
 def _need(t: torch.Tensor | None, name: str, dtype=torch.bfloat16, allow_none=False) -> int | None:
     if t is None:
         if allow_none:
@@ -43,9 +96,13 @@ def gemm(a: torch.Tensor, w: torch.Tensor, w_kmajor: bool = True, out: torch.Ten
         raise ValueError(f"gemm: weight {tuple(w.shape)} does not match K={K}")
     if out is None:
         out = torch.empty((M, N), dtype=torch.bfloat16, device=a.device)
+    t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_gemm_bf16(
         _stream(), M, N, K, _need(a, "a"), _need(w, "w"), int(w_kmajor), _need(out, "out"),
         out.stride(0), _need(residual, "residual", allow_none=True)), "plora_gemm_bf16")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        _TIMER.stop("gemm", t, flops=2.0 * M * N * K)
     return out
 
 
@@ -62,11 +119,42 @@ def linear_fwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
     if y_out is None:
         y_out = torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
     s = meta.struct
+    if _TIMER is not None:
+        shrink(meta, x, a_sh, hs_out)
+        linear_expand(meta, x, w, w_kmajor, bt_sh, hs_out, y_out, residual)
+        return y_out, hs_out
     _lib.check(_lib.lib().plora_linear_fwd(
         _stream(), ctypes.byref(s), _need(x, "x"), d, k, _need(w, "w"), int(w_kmajor),
         _need(a_sh, "a_sh"), _need(bt_sh, "bt_sh"), _need(hs_out, "hs_out"), _need(y_out, "y"),
         y_out.stride(0), _need(residual, "residual", allow_none=True)), "plora_linear_fwd")
+    _LAUNCHES[0] += 2
     return y_out, hs_out
+
+
+def shrink(meta: PackMeta, p: torch.Tensor, l_sh: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """K2a / K4: out = alpha_i * p_i @ L_i  (L_sh [n][K][rpad64])."""
+    T, K = p.shape
+    t = _TIMER.start() if _TIMER else None
+    _lib.check(_lib.lib().plora_lora_shrink(_stream(), ctypes.byref(meta.struct), K, _need(p, "p"),
+                                            _need(l_sh, "l_sh"), _need(out, "out")), "plora_lora_shrink")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("shrink", t, flops=2.0 * K * tr, nbytes=2.0 * T * K + 2.0 * K * R + 2.0 * tr)
+    return out
+
+
+def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    """K3 / K5: G_i = p_i^T q_i per token segment, fp32 into the adapter-major region g."""
+    T, Mdim = p.shape
+    t = _TIMER.start() if _TIMER else None
+    _lib.check(_lib.lib().plora_lora_segred(_stream(), ctypes.byref(meta.struct), Mdim, _need(p, "p"),
+                                            _need(q, "q"), _need(g, "g", torch.float32)), "plora_lora_segred")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr, nbytes=2.0 * T * Mdim + 2.0 * tr + 4.0 * Mdim * R)
+    return g
 
 
 def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
@@ -78,10 +166,15 @@ def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bo
     if y_out is None:
         y_out = torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
     s = meta.struct
+    t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_linear_expand(
         _stream(), ctypes.byref(s), _need(x, "x"), d, k, _need(w, "w"), int(w_kmajor),
         _need(bt_sh, "bt_sh"), _need(hs, "hs"), _need(y_out, "y"), y_out.stride(0),
         _need(residual, "residual", allow_none=True)), "plora_linear_expand")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("gemm", t, flops=2.0 * T * d * k + 2.0 * k * tr)
     return y_out
 
 
@@ -89,7 +182,7 @@ def linear_bwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
                a_sh: torch.Tensor, bt_sh: torch.Tensor, hs: torch.Tensor, dy: torch.Tensor,
                grad_a: torch.Tensor | None, grad_b: torch.Tensor | None,
                dx_out: torch.Tensor | None = None, need_dx: bool = True,
-               dh_ws: torch.Tensor | None = None):
+               dh_ws: torch.Tensor | None = None, dx_residual: torch.Tensor | None = None):
     """Packed LoRA linear backward (Cases 1-4).  Writes fp32 grads into grad_a /
     grad_b (adapter-major regions) and returns dx (or None)."""
     T, d = x.shape
@@ -99,11 +192,22 @@ def linear_bwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
     if need_dx and dx_out is None:
         dx_out = torch.empty((T, d), dtype=torch.bfloat16, device=x.device)
     s = meta.struct
+    if _TIMER is not None:
+        shrink(meta, dy, bt_sh, dh_ws)                       # Case 2 (K4)
+        if grad_b is not None:
+            segred(meta, dy, hs, grad_b)                     # Case 1 (K3)
+        if grad_a is not None:
+            segred(meta, x, dh_ws, grad_a)                   # Case 3 (K5)
+        if need_dx:                                          # Case 4 (K6): dX = dY op(W)^T + dH A^T
+            linear_expand(meta, dy, w, not w_kmajor, a_sh, dh_ws, dx_out, dx_residual)
+        return dx_out if need_dx else None
+    _LAUNCHES[0] += 1 + (grad_a is not None) + (grad_b is not None) + bool(need_dx)
     _lib.check(_lib.lib().plora_linear_bwd(
         _stream(), ctypes.byref(s), _need(x, "x"), d, k, _need(w, "w"), int(w_kmajor),
         _need(a_sh, "a_sh"), _need(bt_sh, "bt_sh"), _need(hs, "hs"), _need(dy, "dy"),
         _need(dh_ws, "dh_ws"), _need(dx_out, "dx", allow_none=True) if need_dx else None,
         dx_out.stride(0) if (need_dx and dx_out is not None) else 0,
+        _need(dx_residual, "dx_residual", allow_none=True) if need_dx else None,
         _need(grad_a, "grad_a", torch.float32, allow_none=True),
         _need(grad_b, "grad_b", torch.float32, allow_none=True)), "plora_linear_bwd")
     return dx_out if need_dx else None
@@ -111,11 +215,16 @@ def linear_bwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
 
 def adamw(chunks: torch.Tensor, param: torch.Tensor, grad: torch.Tensor, exp_avg: torch.Tensor,
           exp_avg_sq: torch.Tensor, shadow: torch.Tensor, hp: torch.Tensor, step: int,
-          beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
+          beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, algo_params: int | None = None) -> None:
     """Fused per-adapter AdamW over the chunk table (see include/plora.h)."""
+    _LAUNCHES[0] += 1
+    t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_adamw(
         _stream(), chunks.shape[0], _need(chunks, "chunks", torch.int64),
         _need(param, "param", torch.float32), _need(grad, "grad", torch.float32),
         _need(exp_avg, "exp_avg", torch.float32), _need(exp_avg_sq, "exp_avg_sq", torch.float32),
         _need(shadow, "shadow"), _need(hp, "hp", torch.float32), beta1, beta2, eps, int(step)),
         "plora_adamw")
+    if t is not None:
+        # 30 B per trainable parameter: read p,g,m,v (16) + write p,m,v (12) + bf16 shadow (2)
+        _TIMER.stop("adamw", t, nbytes=30.0 * (algo_params if algo_params is not None else param.numel()))
