@@ -54,7 +54,7 @@ class AdapterBank:
     def __init__(self, meta: PackMeta, n_layers: int, targets: Sequence[Target], lrs: Sequence[float],
                  weight_decay: float | Sequence[float] = 0.0, device="cuda",
                  betas=(0.9, 0.999), eps: float = 1e-8, seeds: Sequence[int] | None = None,
-                 init: str = "bench", a_scale: float | None = None, b_std: float = 0.02,
+                 init: str = "bench", a_scale: float | None = None, b_std: float | Sequence[float] = 0.02,
                  chunk_elems: int = 8192):
         self.meta = meta
         self.n = meta.n_adapters
@@ -142,6 +142,7 @@ class AdapterBank:
         """A_i ~ U(+-1/sqrt(h_in)), B_i ~ N(0, b_std^2) (nonzero, so Case 3 is exercised
         from step 1), seeded per adapter."""
         m = self.meta
+        b_stds = [float(b_std)] * self.n if np.isscalar(b_std) else [float(b) for b in b_std]
         for i, seed in enumerate(seeds):
             g = torch.Generator(device=self.device).manual_seed(int(seed))
             for layer in range(self.n_layers):
@@ -149,7 +150,7 @@ class AdapterBank:
                     r = m.ranks[i]
                     bound = a_scale if a_scale is not None else 1.0 / math.sqrt(t.h_in)
                     a = (torch.rand(t.h_in, r, generator=g, device=self.device) * 2 - 1) * bound
-                    b = torch.randn(t.h_out, r, generator=g, device=self.device) * b_std
+                    b = torch.randn(t.h_out, r, generator=g, device=self.device) * b_stds[i]
                     self.block(self.P, layer, t.name, "A", i)[:, :r] = a
                     self.block(self.P, layer, t.name, "B", i)[:, :r] = b
         self.refresh_shadow()

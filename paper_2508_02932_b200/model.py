@@ -190,7 +190,7 @@ class PackedLoraTrainer:
 
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
-                 a_scale: float | None = None, b_std: float = 0.02):
+                 a_scale: float | None = None, b_std: float | Sequence[float] = 0.02):
         self.cfg = cfg
         self.specs = list(specs)
         self.s = seq_len

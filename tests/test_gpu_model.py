@@ -4,8 +4,8 @@ oracle restatement of lorasweep.packed_forward/packed_backward.
 
 Tolerance tier (bf16 activations end to end, fp32 accumulation / fp32 grads):
   per-adapter loss   |d| / |ref| <= 1e-2
-  per-(layer, target, adapter) LoRA gradient: relative Frobenius <= 5e-2
-  (all gradients pooled: relative Frobenius <= 2e-2)"""
+  per-(layer, target, adapter) LoRA gradient: relative Frobenius <= 2e-2
+  (all gradients pooled: relative Frobenius <= 1.5e-2)"""
 
 import numpy as np
 import pytest
@@ -19,10 +19,16 @@ pytestmark = pytest.mark.gpu
 
 
 def _trainer(specs=None, seeds=None):
+    """C1 with the bench ranks/alphas (alpha = r * {0.25,1,2,4} up to 256).  B_i is drawn
+    with std 0.2/alpha_i so every adapter's low-rank term is O(1) next to the base path:
+    with B ~ N(0, 0.05^2) the alpha=256 adapter's term is ~100x the base output, the
+    random-weight network saturates its attention and the bf16-vs-fp64 comparison
+    measures chaos, not the kernels."""
     cfg = PRESETS["tiny"]
     sp, s = bench_adapters("tiny")
     specs = specs or sp
-    return PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=seeds, a_scale=0.05, b_std=0.05)
+    return PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=seeds, a_scale=0.05,
+                             b_std=[0.2 / x.alpha for x in specs])
 
 
 def _oracle(tr, tokens):
@@ -56,8 +62,8 @@ def test_tiny_model_matches_oracle():
                 den += rn * rn
                 worst = max(worst, e / max(rn, 1e-30))
     print("worst per-block grad rel-Frob", worst, "pooled", (num / den) ** 0.5)
-    assert worst <= 5e-2
-    assert (num / den) ** 0.5 <= 2e-2
+    assert worst <= 2e-2
+    assert (num / den) ** 0.5 <= 1.5e-2
 
 
 def test_padding_columns_stay_zero_after_steps():
@@ -91,7 +97,7 @@ def test_packing_invariance_model_level():
     lp = packed.forward_backward(tokens).clone()
     i = 2
     solo = PackedLoraTrainer(PRESETS["tiny"], [cfg_specs[i]], s, device="cuda", base=packed.base,
-                             adapter_seeds=[100 + i], a_scale=0.05, b_std=0.05)
+                             adapter_seeds=[100 + i], a_scale=0.05, b_std=[0.2 / cfg_specs[i].alpha])
     ro = packed.meta.row_offsets
     ls = solo.forward_backward(tokens[ro[i]:ro[i + 1]].contiguous())
     assert abs(ls[0].item() - lp[i].item()) <= 1e-3 * abs(lp[i].item())
