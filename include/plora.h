@@ -156,6 +156,30 @@ PLORA_API int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks,
                 void* shadow, const float* hp, float beta1, float beta2, float eps,
                 int64_t step);
 
+/* ---- fused HBM-bound helpers of the decoder step (off the LoRA hot path) ---- */
+
+/* y = x * rstd * w with rstd = rsqrt(mean(x^2) + eps) (use_given_rstd = 0 computes
+ * and stores rstd[rows]; 1 recomputes y from a saved rstd).  bf16 [rows][d], d <= 8192. */
+PLORA_API int plora_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const void* x, const void* w,
+                                float eps, void* y, float* rstd, int32_t use_given_rstd);
+/* dx = rstd * (g - xhat * mean(g * xhat)) (+ residual), g = dy * w. */
+PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const void* dy, const void* x,
+                                const float* rstd, const void* w, const void* residual, void* dx);
+/* a = silu(g) * u ;  (dg, du) from da. n elements, multiple of 8. */
+PLORA_API int plora_swiglu_fwd(void* stream, int64_t n, const void* g, const void* u, void* a);
+PLORA_API int plora_swiglu_bwd(void* stream, int64_t n, const void* da, const void* g, const void* u,
+                               void* dg, void* du);
+/* out[t][h][:] = rope(in[b][h][p][:]) (t = b*s + p; element strides sb, sp, sh), half
+ * rotation with cos/sin [s][hd/2] f32; inverse = 1 rotates by -theta (backward);
+ * rotate = 0 performs only the layout change.  out is contiguous [T][H][hd]. */
+PLORA_API int plora_rope(void* stream, const void* in, void* out, const float* cosv, const float* sinv,
+                         int64_t T, int32_t s, int32_t H, int32_t hd, int64_t sb, int64_t sp, int64_t sh,
+                         int32_t rotate, int32_t inverse);
+/* Weighted cross entropy over bf16 logits [rows][V] (overwritten with the gradient
+ * weight_t * (softmax_t - onehot_t)); tok_loss[t] = weight_t * CE_t. */
+PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* logits,
+                                  const int64_t* labels, const float* weight, float* tok_loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,12 @@ EXPORTS = (
     "plora_linear_expand",
     "plora_linear_bwd",
     "plora_adamw",
+    "plora_rmsnorm_fwd",
+    "plora_rmsnorm_bwd",
+    "plora_swiglu_fwd",
+    "plora_swiglu_bwd",
+    "plora_rope",
+    "plora_cross_entropy",
 )
 
 ABI_VERSION = 1
@@ -81,6 +87,13 @@ _SIGNATURES = {
                           _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_adamw": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _i64],
                     ctypes.c_int),
+    "plora_rmsnorm_fwd": ([_vp, _i64, _i64, _vp, _vp, _f32, _vp, _vp, _i32], ctypes.c_int),
+    "plora_rmsnorm_bwd": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "plora_swiglu_fwd": ([_vp, _i64, _vp, _vp, _vp], ctypes.c_int),
+    "plora_swiglu_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "plora_rope": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _i32],
+                   ctypes.c_int),
+    "plora_cross_entropy": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp], ctypes.c_int),
 }
 
 

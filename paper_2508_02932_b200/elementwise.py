@@ -1,30 +1,105 @@
 """Non-GEMM ops of the decoder step (off the packed-LoRA hot path).
 
-RMSNorm, RoPE, SwiGLU and the chunked cross-entropy are small HBM-bound passes.
-They dispatch to fused sm_100a kernels in libplora when available (``fused``)
-and are otherwise written in plain torch (which also serves as the fp32
-reference for the fused kernels' tests).
+RMSNorm, RoPE, SwiGLU and the chunked cross-entropy are small HBM-bound passes
+run by fused sm_100a kernels in libplora (csrc/elementwise.cu).  The ``ref_*``
+functions are plain-torch fp32 restatements used only by the tests as the
+reference for those kernels; the model never calls them.
 """
 
 from __future__ import annotations
 
 import torch
 
+from . import _lib
+from .ops import _LAUNCHES, _need, _stream
+
 bf16 = torch.bfloat16
 
 
 def rmsnorm_fwd(x: torch.Tensor, w: torch.Tensor, eps: float):
+    rows, d = x.shape
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib().plora_rmsnorm_fwd(_stream(), rows, d, _need(x, "x"), _need(w, "w"), eps,
+                                            _need(y, "y"), _need(rstd, "rstd", torch.float32), 0), "rmsnorm_fwd")
+    _LAUNCHES[0] += 1
+    return y, rstd
+
+
+def rmsnorm_apply(x: torch.Tensor, rstd: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None):
+    rows, d = x.shape
+    y = torch.empty_like(x) if out is None else out
+    _lib.check(_lib.lib().plora_rmsnorm_fwd(_stream(), rows, d, _need(x, "x"), _need(w, "w"), 0.0,
+                                            _need(y, "y"), _need(rstd, "rstd", torch.float32), 1), "rmsnorm_apply")
+    _LAUNCHES[0] += 1
+    return y
+
+
+def rmsnorm_bwd(dy: torch.Tensor, x: torch.Tensor, rstd: torch.Tensor, w: torch.Tensor,
+                residual_grad: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    rows, d = x.shape
+    dx = torch.empty_like(x) if out is None else out
+    _lib.check(_lib.lib().plora_rmsnorm_bwd(_stream(), rows, d, _need(dy, "dy"), _need(x, "x"),
+                                            _need(rstd, "rstd", torch.float32), _need(w, "w"),
+                                            _need(residual_grad, "residual_grad", allow_none=True),
+                                            _need(dx, "dx")), "rmsnorm_bwd")
+    _LAUNCHES[0] += 1
+    return dx
+
+
+def swiglu_fwd(g: torch.Tensor, u: torch.Tensor, out: torch.Tensor | None = None):
+    a = torch.empty_like(g) if out is None else out
+    _lib.check(_lib.lib().plora_swiglu_fwd(_stream(), g.numel(), _need(g, "g"), _need(u, "u"), _need(a, "a")),
+               "swiglu_fwd")
+    _LAUNCHES[0] += 1
+    return a
+
+
+def swiglu_bwd(da: torch.Tensor, g: torch.Tensor, u: torch.Tensor, out_g=None, out_u=None):
+    dg = torch.empty_like(g) if out_g is None else out_g
+    du = torch.empty_like(u) if out_u is None else out_u
+    _lib.check(_lib.lib().plora_swiglu_bwd(_stream(), g.numel(), _need(da, "da"), _need(g, "g"), _need(u, "u"),
+                                           _need(dg, "dg"), _need(du, "du")), "swiglu_bwd")
+    _LAUNCHES[0] += 1
+    return dg, du
+
+
+def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, seq_len: int, out: torch.Tensor | None = None,
+         inverse: bool = False, rotate: bool = True) -> torch.Tensor:
+    """x is a [B, s, H, hd] or [B, H, s, hd]-strided view (given as [B, s, H, hd] dims order
+    via ``bshd``); returns a contiguous [B*s, H*hd] tensor (may be x itself if in place)."""
+    B, s, H, hd = x.shape
+    if x.stride(-1) != 1:
+        raise ValueError("rope: last dim must be contiguous")
+    T = B * s
+    if out is None:
+        out = torch.empty((T, H * hd), dtype=x.dtype, device=x.device)
+    _lib.check(_lib.lib().plora_rope(_stream(), x.data_ptr(), _need(out, "out"),
+                                     _need(cos, "cos", torch.float32), _need(sin, "sin", torch.float32),
+                                     T, s, H, hd, x.stride(0), x.stride(1), x.stride(2), int(rotate),
+                                     int(inverse)), "rope")
+    _LAUNCHES[0] += 1
+    return out
+
+
+def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, weight: torch.Tensor, tok_loss: torch.Tensor):
+    """Overwrites bf16 logits [Tc][V] with weight_t (softmax_t - onehot_t); tok_loss[t] = weight_t CE_t."""
+    rows, V = logits.shape
+    _lib.check(_lib.lib().plora_cross_entropy(_stream(), rows, V, _need(logits, "logits"),
+                                              _need(labels, "labels", torch.int64),
+                                              _need(weight, "weight", torch.float32),
+                                              _need(tok_loss, "tok_loss", torch.float32)), "cross_entropy")
+    _LAUNCHES[0] += 1
+
+
+# ---------------------------------------------------------------------------- torch references
+def ref_rmsnorm_fwd(x, w, eps):
     xf = x.float()
     rstd = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
     return (xf * rstd * w.float()).to(bf16), rstd.squeeze(-1)
 
 
-def rmsnorm_apply(x: torch.Tensor, rstd: torch.Tensor, w: torch.Tensor):
-    return (x.float() * rstd.unsqueeze(-1) * w.float()).to(bf16)
-
-
-def rmsnorm_bwd(dy: torch.Tensor, x: torch.Tensor, rstd: torch.Tensor, w: torch.Tensor,
-                residual_grad: torch.Tensor | None = None):
+def ref_rmsnorm_bwd(dy, x, rstd, w, residual_grad=None):
     r = rstd.unsqueeze(-1)
     xhat = x.float() * r
     g = dy.float() * w.float()
@@ -34,45 +109,29 @@ def rmsnorm_bwd(dy: torch.Tensor, x: torch.Tensor, rstd: torch.Tensor, w: torch.
     return dx.to(bf16)
 
 
-def rope_fwd(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor):
-    """x [B, s, H, hd] (half-rotation convention); cos/sin [s, hd/2]."""
+def ref_rope(x, cos, sin, inverse=False):
+    """x [B, s, H, hd] -> [B, s, H, hd] rotated (half-rotation)."""
     h = x.shape[-1] // 2
     c = cos[None, :, None, :]
-    s = sin[None, :, None, :]
+    s = -sin[None, :, None, :] if inverse else sin[None, :, None, :]
     x1, x2 = x[..., :h].float(), x[..., h:].float()
     return torch.cat((x1 * c - x2 * s, x2 * c + x1 * s), dim=-1).to(bf16)
 
 
-def rope_bwd(dy: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor):
-    h = dy.shape[-1] // 2
-    c = cos[None, :, None, :]
-    s = sin[None, :, None, :]
-    d1, d2 = dy[..., :h].float(), dy[..., h:].float()
-    return torch.cat((d1 * c + d2 * s, d2 * c - d1 * s), dim=-1).to(bf16).contiguous()
-
-
-def swiglu_fwd(g: torch.Tensor, u: torch.Tensor):
+def ref_swiglu_fwd(g, u):
     return (torch.nn.functional.silu(g.float()) * u.float()).to(bf16)
 
 
-def swiglu_bwd(da: torch.Tensor, g: torch.Tensor, u: torch.Tensor):
+def ref_swiglu_bwd(da, g, u):
     gf, uf, daf = g.float(), u.float(), da.float()
     sg = torch.sigmoid(gf)
-    du = daf * gf * sg
-    dg = daf * uf * sg * (1 + gf * (1 - sg))
-    return dg.to(bf16), du.to(bf16)
+    return (daf * uf * sg * (1 + gf * (1 - sg))).to(bf16), (daf * gf * sg).to(bf16)
 
 
-def cross_entropy_fwd_bwd(logits: torch.Tensor, labels: torch.Tensor, weight: torch.Tensor,
-                          token_adapter: torch.Tensor, losses: torch.Tensor) -> None:
-    """Weighted CE over a token chunk.  Overwrites ``logits`` (bf16 [Tc][V]) with
-    d loss / d logits = weight_t * (softmax_t - onehot_t) and adds
-    sum_t weight_t * CE_t into losses[adapter(t)]."""
+def ref_cross_entropy(logits, labels, weight):
     lf = logits.float()
     lse = torch.logsumexp(lf, dim=-1)
-    tgt = lf.gather(1, labels.view(-1, 1)).squeeze(1)
-    losses.index_add_(0, token_adapter, (lse - tgt) * weight)
-    p = torch.exp(lf - lse.unsqueeze(1))
-    p.scatter_add_(1, labels.view(-1, 1), -torch.ones_like(tgt).view(-1, 1))
-    p.mul_(weight.unsqueeze(1))
-    logits.copy_(p.to(bf16))
+    tok = (lse - lf.gather(1, labels.view(-1, 1)).squeeze(1)) * weight
+    p = torch.softmax(lf, dim=-1)
+    p.scatter_add_(1, labels.view(-1, 1), -torch.ones_like(lse).view(-1, 1))
+    return (p * weight.unsqueeze(1)).to(bf16), tok

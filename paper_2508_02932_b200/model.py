@@ -9,8 +9,9 @@ adapters.  The frozen lm_head runs on the same tcgen05 GEMM engine.  The loss is
 sum_i mean_{tokens of i} CE, so every adapter's gradient equals its solo-training
 gradient.
 
-Off the hot path (plain torch / fused helpers in ``elementwise``): embedding
-gather, RMSNorm, RoPE, SwiGLU, attention (torch SDPA), cross-entropy.
+Off the hot path: RMSNorm, RoPE, SwiGLU and cross-entropy run as fused libplora
+kernels (``elementwise``); attention is torch SDPA (cuDNN on B200); the embedding
+gather is a torch index.
 
 The backward is written out explicitly (no autograd tape) so that exactly the
 tensors listed in ``_LayerSave`` are kept: per layer the residual input, the
@@ -214,6 +215,7 @@ class PackedLoraTrainer:
         self.has_label = pos != seq_len - 1
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
+        self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
     def _lin_fwd(self, layer: int, tname: str, x: torch.Tensor, w: torch.Tensor, residual=None):
@@ -233,28 +235,30 @@ class PackedLoraTrainer:
     # ------------------------------------------------------------------ forward
     def _layer_fwd(self, layer: int, h: torch.Tensor) -> tuple[torch.Tensor, _LayerSave]:
         cfg, lw = self.cfg, self.base.layers[layer]
-        T, hd, H, KV = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv
-        B = T // self.s
+        T, hd, H, KV, s = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv, self.s
+        B = T // s
         x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
         q, hs_q = self._lin_fwd(layer, "q", x1, lw["q"])
         k, hs_k = self._lin_fwd(layer, "k", x1, lw["k"])
         v, hs_v = self._lin_fwd(layer, "v", x1, lw["v"])
+        del x1
         if cfg.qkv_bias:
             q += lw["q_bias"]
             k += lw["k_bias"]
             v += lw["v_bias"]
-        q = ew.rope_fwd(q.view(B, self.s, H, hd), self.cos, self.sin)
-        k = ew.rope_fwd(k.view(B, self.s, KV, hd), self.cos, self.sin)
-        qg = q.transpose(1, 2).detach().requires_grad_()
-        kg = k.transpose(1, 2).detach().requires_grad_()
-        vg = v.view(B, self.s, KV, hd).transpose(1, 2).detach().requires_grad_()
+        ew.rope(q.view(B, s, H, hd), self.cos, self.sin, s, out=q)        # in place
+        ew.rope(k.view(B, s, KV, hd), self.cos, self.sin, s, out=k)
+        qg = q.view(B, s, H, hd).transpose(1, 2).detach().requires_grad_()
+        kg = k.view(B, s, KV, hd).transpose(1, 2).detach().requires_grad_()
+        vg = v.view(B, s, KV, hd).transpose(1, 2).detach().requires_grad_()
         with torch.enable_grad():
             og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
-        attn = og.detach().transpose(1, 2).reshape(T, H * hd)
+        attn = ew.rope(og.detach().transpose(1, 2), self.cos, self.sin, s, rotate=False)   # [T][H*hd]
         h_mid, hs_o = self._lin_fwd(layer, "o", attn, lw["o"], residual=h)
         x2, rstd2 = ew.rmsnorm_fwd(h_mid, lw["mlp_norm"], cfg.norm_eps)
         g, hs_g = self._lin_fwd(layer, "gate", x2, lw["gate"])
         u, hs_u = self._lin_fwd(layer, "up", x2, lw["up"])
+        del x2
         act = ew.swiglu_fwd(g, u)
         h_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"], residual=h_mid)
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
@@ -265,29 +269,27 @@ class PackedLoraTrainer:
     # ------------------------------------------------------------------ backward
     def _layer_bwd(self, layer: int, sv: _LayerSave, dh: torch.Tensor, need_dx: bool) -> torch.Tensor:
         cfg, lw = self.cfg, self.base.layers[layer]
-        T, hd, H, KV = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv
-        B = T // self.s
+        T, hd, H, KV, s = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv, self.s
+        B = T // s
         # MLP: h_out = h_mid + down(swiglu(gate(x2), up(x2)))
-        act = ew.swiglu_fwd(sv.g, sv.u)
+        act = ew.swiglu_fwd(sv.g, sv.u)                                   # recompute
         d_act = self._lin_bwd(layer, "down", act, lw["down"], sv.hs["down"], dh)
-        del act
-        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u)
+        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u)  # in place over g, u
         del d_act
         x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
+        del act
         dx2 = self._lin_bwd(layer, "up", x2, lw["up"], sv.hs["up"], du)
         dx2 = self._lin_bwd(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
-        del dg, du
-        d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh)
-        del dx2, x2
+        del dg, du, x2
+        d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh, out=dx2)
         # attention: h_mid = h_in + o(attn(rope(q(x1)), rope(k(x1)), v(x1)))
         d_attn = self._lin_bwd(layer, "o", sv.attn_out, lw["o"], sv.hs["o"], d_mid)
         qg, kg, vg, og = sv.attn_graph
-        dog = d_attn.view(B, self.s, H, hd).transpose(1, 2)
-        dq, dk, dv = torch.autograd.grad(og, (qg, kg, vg), dog)
-        del d_attn, dog
-        dq = ew.rope_bwd(dq.transpose(1, 2), self.cos, self.sin).reshape(T, H * hd)
-        dk = ew.rope_bwd(dk.transpose(1, 2), self.cos, self.sin).reshape(T, KV * hd)
-        dv = dv.transpose(1, 2).reshape(T, KV * hd)
+        dq, dk, dv = torch.autograd.grad(og, (qg, kg, vg), d_attn.view(B, s, H, hd).transpose(1, 2))
+        del d_attn
+        dq = ew.rope(dq.transpose(1, 2), self.cos, self.sin, s, inverse=True)      # [T][H*hd]
+        dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
+        dv = ew.rope(dv.transpose(1, 2), self.cos, self.sin, s, rotate=False)
         x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
         dx1 = self._lin_bwd(layer, "v", x1, lw["v"], sv.hs["v"], dv)
         dx1 = self._lin_bwd(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1)
@@ -295,25 +297,29 @@ class PackedLoraTrainer:
         del dq, dk, dv, x1
         if not need_dx:
             return None
-        return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid)
+        return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid, out=dx1)
 
     # ------------------------------------------------------------------ loss head
     def _head(self, h: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
         """Final norm + lm_head + per-adapter-mean CE, chunked over tokens; returns d h.
-        Accumulates per-adapter losses into self.losses."""
+        Writes per-adapter losses into self.losses."""
         cfg = self.cfg
         xf, rstd = ew.rmsnorm_fwd(h, self.base.final_norm, cfg.norm_eps)
         dxf = torch.empty_like(xf)
         labels = torch.roll(tokens, -1)
-        self.losses.zero_()
+        tok_loss = torch.empty(self.T, dtype=torch.float32, device=self.device)
         for c0 in range(0, self.T, self.ce_chunk):
             c1 = min(self.T, c0 + self.ce_chunk)
             logits = ops.gemm(xf[c0:c1], self.base.lm_head, True)
-            ew.cross_entropy_fwd_bwd(logits, labels[c0:c1], self.ce_weight[c0:c1],
-                                     self.token_adapter[c0:c1], self.losses)
+            ew.cross_entropy(logits, labels[c0:c1], self.ce_weight[c0:c1], tok_loss[c0:c1])
             ops.gemm(logits, self.base.lm_head, False, out=dxf[c0:c1])   # dX = dlogits @ W_lm
             del logits
-        return ew.rmsnorm_bwd(dxf, h, rstd, self.base.final_norm)
+        # per-adapter sums over contiguous segments (deterministic prefix-sum differences)
+        cs = torch.cumsum(tok_loss.double(), 0)
+        cs = torch.cat((cs.new_zeros(1), cs))
+        ro = self._row_off_dev
+        self.losses.copy_((cs[ro[1:]] - cs[ro[:-1]]).float())
+        return ew.rmsnorm_bwd(dxf, h, rstd, self.base.final_norm, out=dxf)
 
     # ------------------------------------------------------------------ step
     def forward_backward(self, tokens: torch.Tensor) -> torch.Tensor:
