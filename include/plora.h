@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 1
+#define PLORA_ABI_VERSION 2
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -63,6 +63,9 @@ typedef struct plora_pack {
   const int32_t* d_ranks;  /* [n]   r_i */
   const int32_t* d_rpad_off;/*[n+1] prefix sums of rpad16_i */
   const float*   d_alpha;  /* [n]   raw alpha_i (no alpha/r) */
+  int32_t n_ptiles;        /* entries in d_ptiles */
+  int32_t pad_;
+  const int32_t* d_ptiles; /* [n_ptiles][4] = {m0, m_len (1..256), adapter, 0}: CTA-pair tiles */
 } plora_pack_t;
 
 /* Library / error plumbing. */
@@ -76,13 +79,14 @@ PLORA_API int plora_device_check(void);   /* 0 iff an sm_100 device is current *
  *   Outputs (caller-allocated host arrays):
  *     rank_off[n+1], row_off[n+1], rpad_off[n+1]
  *     mtiles[max_mtiles][4]  (tile list: every tile lies inside one segment)
+ *     ptiles[max_mtiles][4]  (256-row CTA-pair tiles, same rule; may be NULL)
  *     token_adapter[T]       (may be NULL)
  *   *n_mtiles receives the tile count; if it exceeds max_mtiles nothing is
  *   written to mtiles and status 2 is returned. */
 PLORA_API int plora_meta_build(int32_t n, const int64_t* ranks, const int64_t* tokens,
                      int64_t* rank_off, int64_t* row_off, int32_t* rpad_off,
                      int32_t* mtiles, int32_t max_mtiles, int32_t* n_mtiles,
-                     int32_t* token_adapter);
+                     int32_t* ptiles, int32_t* n_ptiles, int32_t* token_adapter);
 
 /* Upper bound on the tile count for plora_meta_build. */
 PLORA_API int32_t plora_meta_max_mtiles(int32_t n, const int64_t* tokens);

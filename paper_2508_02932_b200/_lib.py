@@ -36,7 +36,7 @@ EXPORTS = (
     "plora_cross_entropy",
 )
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class PloraError(RuntimeError):
@@ -57,6 +57,9 @@ class PackStruct(ctypes.Structure):
         ("d_ranks", ctypes.c_void_p),
         ("d_rpad_off", ctypes.c_void_p),
         ("d_alpha", ctypes.c_void_p),
+        ("n_ptiles", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("d_ptiles", ctypes.c_void_p),
     ]
 
 
@@ -74,7 +77,8 @@ _SIGNATURES = {
     "plora_abi_version": ([], ctypes.c_int),
     "plora_last_error": ([], ctypes.c_char_p),
     "plora_device_check": ([], ctypes.c_int),
-    "plora_meta_build": ([_i32, _p64, _p64, _p64, _p64, _p32, _p32, _i32, _p32, _p32], ctypes.c_int),
+    "plora_meta_build": ([_i32, _p64, _p64, _p64, _p64, _p32, _p32, _i32, _p32, _p32, _p32, _p32],
+                         ctypes.c_int),
     "plora_meta_max_mtiles": ([_i32, _p64], _i32),
     "plora_gemm_bf16": ([_vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_fwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,

@@ -367,4 +367,257 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
   }
 }
 
+// ============================================================================
+// CTA-pair variant of MODE_GEMM (K1 + K2b forward, K6 dX): a cluster of 2 CTAs on
+// one TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256).
+// Each CTA stages its own 128 rows of A and its half (128 columns) of B per K-block
+// (32 KB/stage, 6 stages) -- half the per-SM operand traffic of the 1-CTA kernel.
+// The leader (rank 0) owns the full barriers (TMA bytes of both CTAs land on it),
+// issues the UMMAs and multicasts commits to both CTAs' empty / tmem_full barriers;
+// both CTAs' epilogues drain their own 128 TMEM lanes and arrive on the leader's
+// tmem_empty barrier.  Pair tiles never straddle adapters (meta builder), so the
+// fused LoRA K-steps use one adapter's B_i for all 256 rows.
+struct PairCfg {
+  static constexpr int kBN = 256;
+  static constexpr int kABytes = kBM * kBK * 2;             // 16 KB (own 128 rows)
+  static constexpr int kBBytes = (kBN / 2) * kBK * 2;       // 16 KB (own 128 columns)
+  static constexpr int kStageBytes = kABytes + kBBytes;     // 32 KB
+  static constexpr int kStages = 6;
+  static constexpr int kTmemCols = 512;                     // 2 x 256-column accumulators
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kBand = 8;                           // pair tiles per raster band
+};
+
+struct PairTile {
+  int m0, m_len, adapter, n0, n_main, n_lora, rank;
+};
+
+__device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx) {
+  PairTile t;
+  const int per_band = PairCfg::kBand * a.n_ntiles;
+  const int band = idx / per_band;
+  const int rem = idx - band * per_band;
+  const int g0 = band * PairCfg::kBand;
+  const int bsz = min(PairCfg::kBand, a.n_groups - g0);
+  const int nt = rem / bsz;
+  const int g = g0 + (rem - nt * bsz);
+  if (a.mtiles != nullptr) {
+    const int4 mt = reinterpret_cast<const int4*>(a.mtiles)[g];
+    t.m0 = mt.x;
+    t.m_len = mt.y;
+    t.adapter = mt.z;
+  } else {
+    t.m0 = g * 256;
+    t.m_len = min(256, a.M - t.m0);
+    t.adapter = 0;
+  }
+  t.n0 = nt * PairCfg::kBN;
+  t.n_main = (a.K + kBK - 1) / kBK;
+  if (a.has_lora) {
+    t.rank = a.ranks[t.adapter];
+    t.n_lora = min((t.rank + 63) / 64, a.nb);
+  } else {
+    t.rank = 0;
+    t.n_lora = 0;
+  }
+  return t;
+}
+
+template <bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    plora_gemm_pair_kernel(const __grid_constant__ GemmArgs args) {
+  using Cfg = PairCfg;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const int total = args.n_groups * args.n_ntiles;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&args.tmA);
+    tma_prefetch(&args.tmB);
+    if (args.has_lora) {
+      tma_prefetch(&args.tmH);
+      tma_prefetch(&args.tmL);
+    }
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);   // leader: one arrive.expect_tx per phase (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);  // one multicast commit per phase
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int half = static_cast<int>(rank) * 128;
+      for (int idx = cluster; idx < total; idx += n_clusters) {
+        const PairTile t = decode_pair_tile(args, idx);
+        const int nblk = t.n_main + t.n_lora;
+        for (int b = 0; b < nblk; ++b) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * Cfg::kStageBytes;
+          uint8_t* sB = sA + Cfg::kABytes;
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (b < t.n_main) {
+            const int kc = b * kBK;
+            tma_load_2d_pair(sA, &args.tmA, fb, kc, t.m0 + half);
+            if (B_MN) {
+              tma_load_2d_pair(sB, &args.tmB, fb, t.n0 + half, kc);
+              tma_load_2d_pair(sB + 8192, &args.tmB, fb, t.n0 + half + 64, kc);
+            } else {
+              tma_load_2d_pair(sB, &args.tmB, fb, kc, t.n0 + half);
+            }
+          } else {
+            const int lb = b - t.n_main;
+            tma_load_2d_pair(sA, &args.tmH, fb, lb * 64, t.m0 + half);
+            tma_load_3d_pair(sB, &args.tmL, fb, lb * 64, t.n0 + half, t.adapter);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ UMMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc_main = idesc_bf16(256, Cfg::kBN, false, B_MN);
+      constexpr uint32_t idesc_lora = idesc_bf16(256, Cfg::kBN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int idx = cluster; idx < total; idx += n_clusters) {
+        const PairTile t = decode_pair_tile(args, idx);
+        const int nblk = t.n_main + t.n_lora;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * Cfg::kBN;
+        for (int b = 0; b < nblk; ++b) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            uint8_t* sA = smem + stage * Cfg::kStageBytes;
+            uint8_t* sB = sA + Cfg::kABytes;
+            const uint32_t a0 = smem_u32(sA);
+            const uint32_t b0 = smem_u32(sB);
+            const bool lora = b >= t.n_main;
+            const int ksteps = lora ? min(4, (t.rank - (b - t.n_main) * 64 + 15) / 16) : 4;
+            for (int ks = 0; ks < ksteps; ++ks) {
+              const uint64_t ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
+              uint64_t bd;
+              if (!lora && B_MN) bd = smem_desc_sw128(b0 + ks * 2048, 8192, 1024);
+              else               bd = smem_desc_sw128(b0 + ks * 32, 16, 1024);
+              umma_bf16_pair(d_tmem, ad, bd, lora ? idesc_lora : idesc_main, (b > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma_commit_pair_mc(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+        __syncwarp();
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int idx = cluster; idx < total; idx += n_clusters) {
+      const PairTile t = decode_pair_tile(args, idx);
+      const int m0 = t.m0 + static_cast<int>(rank) * 128;
+      const int m_len = min(128, t.m_len - static_cast<int>(rank) * 128);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
+      const bool row_ok = row < m_len;
+      const int64_t orow = static_cast<int64_t>(m0 + row) * args.ldo;
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow;
+      const __nv_bfloat16* res = args.residual ? args.residual + orow : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < Cfg::kBN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tb + c * 32, r);
+        tmem_ld_wait();
+        const int col0 = t.n0 + c * 32;
+        if (row_ok && col0 < args.N) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (col0 + 32 <= args.N) {
+            if (res) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint4 rv = *reinterpret_cast<const uint4*>(res + col0 + q * 8);
+                const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const float2 f = __bfloat1622float2(rh[h]);
+                  v[q * 8 + 2 * h] += f.x;
+                  v[q * 8 + 2 * h + 1] += f.y;
+                }
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w;
+              w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+              w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+              w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+              w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+              *reinterpret_cast<uint4*>(o + col0 + q * 8) = w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (col0 + j < args.N) {
+                float x = v[j];
+                if (res) x += __bfloat162float(res[col0 + j]);
+                o[col0 + j] = __float2bfloat16_rn(x);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
 }  // namespace plora

@@ -8,6 +8,7 @@
 //   * mtiles    -- the grouped-GEMM tile list {m0, m_len, adapter, 0}: 128-row
 //                  tiles that never straddle two adapters' token segments, so a
 //                  tile's fused LoRA expand uses exactly one adapter's B_i;
+//   * ptiles    -- the same rule at 256 rows: tiles of the CTA-pair (cta_group::2) GEMM;
 //   * token_adapter -- per-token adapter id (np.repeat(arange(n), diff(row_off))).
 // Empty segments (T_i = 0) are legal (reference lorapack.py:90-91) and produce
 // no tiles; rank 0 is rejected exactly like AdapterWeights/PackedAdapters do
@@ -32,7 +33,7 @@ extern "C" int32_t plora_meta_max_mtiles(int32_t n, const int64_t* tokens) {
 extern "C" int plora_meta_build(int32_t n, const int64_t* ranks, const int64_t* tokens,
                                 int64_t* rank_off, int64_t* row_off, int32_t* rpad_off,
                                 int32_t* mtiles, int32_t max_mtiles, int32_t* n_mtiles,
-                                int32_t* token_adapter) {
+                                int32_t* ptiles, int32_t* n_ptiles, int32_t* token_adapter) {
   if (n <= 0) return plora::set_error("nothing to pack");
   if (!ranks || !tokens || !rank_off || !row_off || !rpad_off || !n_mtiles)
     return plora::set_error("plora_meta_build: NULL argument");
@@ -69,6 +70,20 @@ extern "C" int plora_meta_build(int32_t n, const int64_t* ranks, const int64_t* 
       }
     }
   }
+  int64_t pt = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    for (int64_t m = row_off[i]; m < row_off[i + 1]; m += 256) {
+      if (ptiles) {
+        const int64_t len = row_off[i + 1] - m < 256 ? row_off[i + 1] - m : 256;
+        ptiles[4 * pt + 0] = static_cast<int32_t>(m);
+        ptiles[4 * pt + 1] = static_cast<int32_t>(len);
+        ptiles[4 * pt + 2] = i;
+        ptiles[4 * pt + 3] = 0;
+      }
+      ++pt;
+    }
+  }
+  if (n_ptiles) *n_ptiles = static_cast<int32_t>(pt);
   if (token_adapter) {
     for (int32_t i = 0; i < n; ++i)
       for (int64_t r = row_off[i]; r < row_off[i + 1]; ++r) token_adapter[r] = i;

@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -131,6 +132,60 @@ static int launch(const GemmArgs& args, cudaStream_t stream) {
 
 static int pick_bn(int64_t N) { return N >= 256 ? 256 : (N > 64 ? 128 : 64); }
 
+static bool g_pair_enabled = [] {
+  const char* e = getenv("PLORA_GEMM_PAIR");
+  return !(e && e[0] == '0');
+}();
+
+template <bool B_MN>
+static int launch_pair(const GemmArgs& args, cudaStream_t stream) {
+  auto kern = plora_gemm_pair_kernel<B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmemBytes));
+    configured = true;
+  }
+  const int total = args.n_groups * args.n_ntiles;
+  if (total <= 0) return 0;
+  const int max_clusters = num_sms() / 2;
+  const int clusters = total < max_clusters ? total : max_clusters;
+  kern<<<clusters * 2, kThreads, PairCfg::kSmemBytes, stream>>>(args);
+  PLORA_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// CTA-pair GEMM (N >= 256): 256 x 256 tiles with tcgen05 cta_group::2.
+static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
+                         const void* A, const void* W, int w_kmajor, const void* H, const void* L,
+                         void* Y, int64_t ldy, const void* residual) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc = make_map_2d(&a.tmA, A, K, M, K, 64, kBM);
+  if (rc) return rc;
+  if (w_kmajor) rc = make_map_2d(&a.tmB, W, K, N, K, 64, 128);
+  else          rc = make_map_2d(&a.tmB, W, N, K, N, 64, 64);
+  if (rc) return rc;
+  const bool lora = pack != nullptr && H != nullptr && L != nullptr;
+  if (lora) {
+    const int64_t R64 = 64LL * pack->nb;
+    if ((rc = make_map_2d(&a.tmH, H, R64, M, R64, 64, kBM))) return rc;
+    if ((rc = make_map_3d(&a.tmL, L, R64, N, pack->n_adapters, 64, 128))) return rc;
+    a.ranks = pack->d_ranks;
+    a.nb = pack->nb;
+    a.has_lora = 1;
+  }
+  a.mtiles = pack ? pack->d_ptiles : nullptr;
+  a.n_groups = pack ? pack->n_ptiles : static_cast<int>((M + 255) / 256);
+  a.M = static_cast<int>(M);
+  a.N = static_cast<int>(N);
+  a.K = static_cast<int>(K);
+  a.n_ntiles = static_cast<int>((N + 255) / 256);
+  a.out = Y;
+  a.ldo = ldy;
+  a.residual = static_cast<const __nv_bfloat16*>(residual);
+  return w_kmajor ? launch_pair<false>(a, st) : launch_pair<true>(a, st);
+}
+
 // Base GEMM (+ fused LoRA expand).  A: [M][K] K-major.  W: see w_kmajor.
 static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
                     const void* A, const void* W, int w_kmajor, const void* H, const void* L,
@@ -140,6 +195,8 @@ static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_
   if (K % 8 || N % 8 || ldy % 8) return fail("gemm: K, N and ldy must be multiples of 8");
   if (reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16))
     return fail("gemm: output/residual must be 16-byte aligned");
+  if (g_pair_enabled && N >= 256 && (pack == nullptr || pack->d_ptiles != nullptr || pack->n_ptiles == 0))
+    return run_gemm_pair(st, pack, M, N, K, A, W, w_kmajor, H, L, Y, ldy, residual);
   const int BN = pick_bn(N);
   GemmArgs a;
   memset(&a, 0, sizeof(a));

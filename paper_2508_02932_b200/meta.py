@@ -30,6 +30,7 @@ class PackMeta:
     row_offsets: tuple[int, ...]
     rpad_off: np.ndarray          # int32 [n+1], prefix sums of roundup(r_i, 16)
     mtiles: np.ndarray            # int32 [n_mtiles, 4]
+    ptiles: np.ndarray            # int32 [n_ptiles, 4]  (256-row CTA-pair tiles)
     token_adapter: np.ndarray     # int32 [T]
     nb: int                       # 64-column rank blocks in the bf16 shadows
     device: object = None
@@ -65,6 +66,7 @@ class PackMeta:
             return self
         dev = {
             "mtiles": torch.from_numpy(np.ascontiguousarray(self.mtiles, dtype=np.int32)).to(device),
+            "ptiles": torch.from_numpy(np.ascontiguousarray(self.ptiles, dtype=np.int32)).to(device),
             "row_off": torch.tensor(self.row_offsets, dtype=torch.int64, device=device),
             "ranks": torch.tensor(self.ranks, dtype=torch.int32, device=device),
             "rpad_off": torch.from_numpy(self.rpad_off.astype(np.int32)).to(device),
@@ -81,6 +83,8 @@ class PackMeta:
         s.d_ranks = dev["ranks"].data_ptr()
         s.d_rpad_off = dev["rpad_off"].data_ptr()
         s.d_alpha = dev["alpha"].data_ptr()
+        s.n_ptiles = int(self.ptiles.shape[0])
+        s.d_ptiles = dev["ptiles"].data_ptr() if s.n_ptiles else None
         self._dev = dev
         self._struct = s
         self.device = device
@@ -115,12 +119,15 @@ def build_meta(ranks: Sequence[int], tokens: Sequence[int], alphas: Sequence[flo
     rpad_off = np.zeros(n + 1, dtype=np.int32)
     mtiles = np.zeros((max(max_tiles, 1), 4), dtype=np.int32)
     n_tiles = ctypes.c_int32(0)
+    n_ptiles = ctypes.c_int32(0)
+    ptiles = np.zeros((max(max_tiles, 1), 4), dtype=np.int32)
     total = int(t.sum()) if n else 0
     tok_ad = np.zeros(max(total, 1), dtype=np.int32)
     rc = L.plora_meta_build(n, r.ctypes.data_as(p64), t.ctypes.data_as(p64),
                             rank_off.ctypes.data_as(p64), row_off.ctypes.data_as(p64),
                             rpad_off.ctypes.data_as(p32), mtiles.ctypes.data_as(p32),
-                            max(max_tiles, 1), ctypes.byref(n_tiles), tok_ad.ctypes.data_as(p32))
+                            max(max_tiles, 1), ctypes.byref(n_tiles), ptiles.ctypes.data_as(p32),
+                            ctypes.byref(n_ptiles), tok_ad.ctypes.data_as(p32))
     if rc != 0:
         raise ValueError(L.plora_last_error().decode())
     max_rank = int(r.max())
@@ -134,6 +141,7 @@ def build_meta(ranks: Sequence[int], tokens: Sequence[int], alphas: Sequence[flo
         row_offsets=tuple(int(x) for x in row_off),
         rpad_off=rpad_off,
         mtiles=mtiles[: n_tiles.value].copy(),
+        ptiles=ptiles[: n_ptiles.value].copy(),
         token_adapter=tok_ad[:total].copy(),
         nb=nb,
     )

@@ -82,6 +82,30 @@ def test_packed_linear_vs_torch(kmajor, d, k):
         assert not torch.any(blk_a[:, r:]) and not torch.any(blk_b[:, r:])   # padding stays zero
 
 
+@pytest.mark.parametrize("kmajor", [True, False])
+def test_unaligned_segments_pair_tiles(kmajor):
+    """Segments that are not multiples of 128/256 rows (odd CTA-pair tiles, a 5-token
+    segment, an empty one) through the CTA-pair GEMM (N >= 256) and the 1-CTA kernels."""
+    ranks, tokens = [8, 64, 16, 32, 40], [300, 5, 0, 129, 700]
+    d, k = 320, 512
+    meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, k, seed=77, kmajor=kmajor)
+    y, hs = ops.linear_fwd(meta, x, w, kmajor, a_sh, bt_sh)
+    ga = torch.empty(d * meta.rpad16_total, device="cuda")
+    gb = torch.empty(k * meta.rpad16_total, device="cuda")
+    dx = ops.linear_bwd(meta, x, w, kmajor, a_sh, bt_sh, hs, dy, ga, gb)
+    ry, rdx, rdA, rdB = reference(meta, x, w, kmajor, a_sh, bt_sh, dy)
+    assert rel(y, ry) < 1e-2 and rel(dx, rdx) < 1e-2
+    for i, r in enumerate(ranks):
+        rp = int(meta.rpad_off[i + 1] - meta.rpad_off[i])
+        blk_a = ga[d * int(meta.rpad_off[i]): d * int(meta.rpad_off[i + 1])].view(d, rp)
+        blk_b = gb[k * int(meta.rpad_off[i]): k * int(meta.rpad_off[i + 1])].view(k, rp)
+        if tokens[i] == 0:
+            assert not torch.any(blk_a) and not torch.any(blk_b)
+            continue
+        assert rel(blk_a[:, :r], rdA[i]) < 5e-3, ("dA", i)
+        assert rel(blk_b[:, :r], rdB[i]) < 5e-3, ("dB", i)
+
+
 def test_packing_invariance():
     """Adapter i's outputs/grads in a pack equal running it alone."""
     d, k = 1024, 2048

@@ -34,6 +34,12 @@ def _check_tiles(m):
         assert so[a] <= m0 and m0 + ln <= so[a + 1]   # never straddles two segments
         covered[m0:m0 + ln] += 1
     assert (covered == 1).all()
+    covered[:] = 0
+    for m0, ln, a, z in m.ptiles:
+        assert z == 0 and 1 <= ln <= 256
+        assert so[a] <= m0 and m0 + ln <= so[a + 1]
+        covered[m0:m0 + ln] += 1
+    assert (covered == 1).all()
 
 
 def test_random_packs_match_oracle_prefix_sums():
@@ -68,3 +74,4 @@ def test_bench_config_tiles():
     m = build_meta([8, 16, 32, 64] * 4, [x * 1024 for x in b], [1.0] * 16)
     assert m.total_tokens == 32768
     assert len(m.mtiles) == 256 and (m.mtiles[:, 1] == 128).all()
+    assert len(m.ptiles) == 128 and (m.ptiles[:, 1] == 256).all()
