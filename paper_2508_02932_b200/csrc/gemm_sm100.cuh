@@ -47,6 +47,7 @@ struct __align__(64) GemmArgs {
   int32_t mt_per;    // SEGRED: ceil(M/128)
   int32_t has_lora;
   int32_t nb;        // 64-column rank blocks
+  int32_t debug;     // bit 0: skip epilogue stores (profiling experiments only)
 };
 
 constexpr int kBM = 128;
@@ -369,21 +370,25 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
 
 // ============================================================================
 // CTA-pair variant of MODE_GEMM (K1 + K2b forward, K6 dX): a cluster of 2 CTAs on
-// one TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256).
-// Each CTA stages its own 128 rows of A and its half (128 columns) of B per K-block
-// (32 KB/stage, 6 stages) -- half the per-SM operand traffic of the 1-CTA kernel.
-// The leader (rank 0) owns the full barriers (TMA bytes of both CTAs land on it),
-// issues the UMMAs and multicasts commits to both CTAs' empty / tmem_full barriers;
-// both CTAs' epilogues drain their own 128 TMEM lanes and arrive on the leader's
-// tmem_empty barrier.  Pair tiles never straddle adapters (meta builder), so the
-// fused LoRA K-steps use one adapter's B_i for all 256 rows.
+// one TPC computes a 256 x (256*NB) tile with tcgen05.mma.cta_group::2 (M = 256).
+// Each CTA stages its own 128 rows of A and its half of every 256-column chunk of B
+// per K-block (16 KB + NB x 16 KB per stage).  NB = 2 (256 x 512 tiles) moves 25%
+// fewer operand bytes per FLOP than NB = 1 -- L2->SMEM bandwidth (~10 TB/s measured)
+// is what bounds this kernel -- at the price of a single (not double-buffered)
+// 512-column TMEM accumulator.  The leader (rank 0) owns the full barriers (TMA
+// bytes of both CTAs land on it), issues the UMMAs and multicasts commits to both
+// CTAs' empty / tmem_full barriers; both CTAs' epilogues drain their own 128 TMEM
+// lanes and arrive on the leader's tmem_empty barrier.  Pair tiles never straddle
+// adapters (meta builder), so the fused LoRA K-steps use one adapter's B_i.
+template <int NB>
 struct PairCfg {
-  static constexpr int kBN = 256;
+  static constexpr int kBN = 256 * NB;                      // output columns per pair tile
   static constexpr int kABytes = kBM * kBK * 2;             // 16 KB (own 128 rows)
-  static constexpr int kBBytes = (kBN / 2) * kBK * 2;       // 16 KB (own 128 columns)
-  static constexpr int kStageBytes = kABytes + kBBytes;     // 32 KB
-  static constexpr int kStages = 6;
-  static constexpr int kTmemCols = 512;                     // 2 x 256-column accumulators
+  static constexpr int kBBytes = NB * 128 * kBK * 2;        // own half of each 256-col chunk
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = NB == 1 ? 6 : 4;
+  static constexpr int kAccStages = NB == 1 ? 2 : 1;
+  static constexpr int kTmemCols = 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
   static constexpr int kBand = 8;                           // pair tiles per raster band
 };
@@ -392,13 +397,14 @@ struct PairTile {
   int m0, m_len, adapter, n0, n_main, n_lora, rank;
 };
 
+template <int NB>
 __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx) {
   PairTile t;
-  const int per_band = PairCfg::kBand * a.n_ntiles;
+  const int per_band = PairCfg<NB>::kBand * a.n_ntiles;
   const int band = idx / per_band;
   const int rem = idx - band * per_band;
-  const int g0 = band * PairCfg::kBand;
-  const int bsz = min(PairCfg::kBand, a.n_groups - g0);
+  const int g0 = band * PairCfg<NB>::kBand;
+  const int bsz = min(PairCfg<NB>::kBand, a.n_groups - g0);
   const int nt = rem / bsz;
   const int g = g0 + (rem - nt * bsz);
   if (a.mtiles != nullptr) {
@@ -411,7 +417,7 @@ __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx)
     t.m_len = min(256, a.M - t.m0);
     t.adapter = 0;
   }
-  t.n0 = nt * PairCfg::kBN;
+  t.n0 = nt * PairCfg<NB>::kBN;
   t.n_main = (a.K + kBK - 1) / kBK;
   if (a.has_lora) {
     t.rank = a.ranks[t.adapter];
@@ -423,11 +429,14 @@ __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx)
   return t;
 }
 
-template <bool B_MN>
+__device__ __forceinline__ uint32_t peer_masked(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
+
+template <bool B_MN, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     plora_gemm_pair_kernel(const __grid_constant__ GemmArgs args) {
-  using Cfg = PairCfg;
+  using Cfg = PairCfg<NB>;
   constexpr int S = Cfg::kStages;
+  constexpr int AS = Cfg::kAccStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
@@ -474,27 +483,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       const int half = static_cast<int>(rank) * 128;
       for (int idx = cluster; idx < total; idx += n_clusters) {
-        const PairTile t = decode_pair_tile(args, idx);
+        const PairTile t = decode_pair_tile<NB>(args, idx);
         const int nblk = t.n_main + t.n_lora;
         for (int b = 0; b < nblk; ++b) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * Cfg::kStageBytes;
           uint8_t* sB = sA + Cfg::kABytes;
+          if (args.debug & 2) {  // profiling experiment: no operand traffic
+            if (leader) mbar_arrive(&full_bar[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) mbar_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
-          const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          const uint32_t fb = peer_masked(&full_bar[stage]);
           if (b < t.n_main) {
             const int kc = b * kBK;
             tma_load_2d_pair(sA, &args.tmA, fb, kc, t.m0 + half);
-            if (B_MN) {
-              tma_load_2d_pair(sB, &args.tmB, fb, t.n0 + half, kc);
-              tma_load_2d_pair(sB + 8192, &args.tmB, fb, t.n0 + half + 64, kc);
-            } else {
-              tma_load_2d_pair(sB, &args.tmB, fb, kc, t.n0 + half);
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+              const int n = t.n0 + 256 * c + half;
+              if (B_MN) {
+                tma_load_2d_pair(sB + c * 16384, &args.tmB, fb, n, kc);
+                tma_load_2d_pair(sB + c * 16384 + 8192, &args.tmB, fb, n + 64, kc);
+              } else {
+                tma_load_2d_pair(sB + c * 16384, &args.tmB, fb, kc, n);
+              }
             }
           } else {
             const int lb = b - t.n_main;
             tma_load_2d_pair(sA, &args.tmH, fb, lb * 64, t.m0 + half);
-            tma_load_3d_pair(sB, &args.tmL, fb, lb * 64, t.n0 + half, t.adapter);
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+              tma_load_3d_pair(sB + c * 16384, &args.tmL, fb, lb * 64, t.n0 + 256 * c + half, t.adapter);
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -503,14 +523,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ UMMA issuer (leader only)
     if (leader) {
-      constexpr uint32_t idesc_main = idesc_bf16(256, Cfg::kBN, false, B_MN);
-      constexpr uint32_t idesc_lora = idesc_bf16(256, Cfg::kBN, false, false);
+      constexpr uint32_t idesc_main = idesc_bf16(256, 256, false, B_MN);
+      constexpr uint32_t idesc_lora = idesc_bf16(256, 256, false, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int idx = cluster; idx < total; idx += n_clusters) {
-        const PairTile t = decode_pair_tile(args, idx);
+        const PairTile t = decode_pair_tile<NB>(args, idx);
         const int nblk = t.n_main + t.n_lora;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -527,10 +547,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int ksteps = lora ? min(4, (t.rank - (b - t.n_main) * 64 + 15) / 16) : 4;
             for (int ks = 0; ks < ksteps; ++ks) {
               const uint64_t ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
-              uint64_t bd;
-              if (!lora && B_MN) bd = smem_desc_sw128(b0 + ks * 2048, 8192, 1024);
-              else               bd = smem_desc_sw128(b0 + ks * 32, 16, 1024);
-              umma_bf16_pair(d_tmem, ad, bd, lora ? idesc_lora : idesc_main, (b > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+              for (int c = 0; c < NB; ++c) {
+                uint64_t bd;
+                if (!lora && B_MN) bd = smem_desc_sw128(b0 + c * 16384 + ks * 2048, 8192, 1024);
+                else               bd = smem_desc_sw128(b0 + c * 16384 + ks * 32, 16, 1024);
+                umma_bf16_pair(d_tmem + 256 * c, ad, bd, lora ? idesc_lora : idesc_main,
+                               (b > 0 || ks > 0) ? 1u : 0u);
+              }
             }
             umma_commit_pair_mc(&empty_bar[stage], 0x3);
           }
@@ -539,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
         __syncwarp();
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == AS) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
@@ -550,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int idx = cluster; idx < total; idx += n_clusters) {
-      const PairTile t = decode_pair_tile(args, idx);
+      const PairTile t = decode_pair_tile<NB>(args, idx);
       const int m0 = t.m0 + static_cast<int>(rank) * 128;
       const int m_len = min(128, t.m_len - static_cast<int>(rank) * 128);
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -561,7 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow;
       const __nv_bfloat16* res = args.residual ? args.residual + orow : nullptr;
 #pragma unroll 1
-      for (int c = 0; c < Cfg::kBN / 32; ++c) {
+      for (int c = 0; c < ((args.debug & 1) ? 0 : Cfg::kBN / 32); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tb + c * 32, r);
         tmem_ld_wait();
@@ -608,7 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == AS) { acc = 0; acc_phase ^= 1; }
     }
   }
 

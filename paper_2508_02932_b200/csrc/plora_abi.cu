@@ -132,32 +132,43 @@ static int launch(const GemmArgs& args, cudaStream_t stream) {
 
 static int pick_bn(int64_t N) { return N >= 256 ? 256 : (N > 64 ? 128 : 64); }
 
+static int g_debug_flags = [] {
+  const char* e = getenv("PLORA_DEBUG_FLAGS");
+  return e ? atoi(e) : 0;
+}();
+
 static bool g_pair_enabled = [] {
   const char* e = getenv("PLORA_GEMM_PAIR");
   return !(e && e[0] == '0');
 }();
 
-template <bool B_MN>
+template <bool B_MN, int NB>
 static int launch_pair(const GemmArgs& args, cudaStream_t stream) {
-  auto kern = plora_gemm_pair_kernel<B_MN>;
+  auto kern = plora_gemm_pair_kernel<B_MN, NB>;
   static bool configured = false;
   if (!configured) {
-    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmemBytes));
+    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<NB>::kSmemBytes));
     configured = true;
   }
   const int total = args.n_groups * args.n_ntiles;
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
   const int clusters = total < max_clusters ? total : max_clusters;
-  kern<<<clusters * 2, kThreads, PairCfg::kSmemBytes, stream>>>(args);
+  kern<<<clusters * 2, kThreads, PairCfg<NB>::kSmemBytes, stream>>>(args);
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
+
+static int g_pair_nb_min_n = [] {   // N at which the 256x512 pair tile is used
+  const char* e = getenv("PLORA_PAIR512_MIN_N");
+  return e ? atoi(e) : 2048;
+}();
 
 // CTA-pair GEMM (N >= 256): 256 x 256 tiles with tcgen05 cta_group::2.
 static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
                          const void* A, const void* W, int w_kmajor, const void* H, const void* L,
                          void* Y, int64_t ldy, const void* residual) {
+  const int NB = N >= g_pair_nb_min_n ? 2 : 1;
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   int rc = make_map_2d(&a.tmA, A, K, M, K, 64, kBM);
@@ -179,11 +190,13 @@ static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, i
   a.M = static_cast<int>(M);
   a.N = static_cast<int>(N);
   a.K = static_cast<int>(K);
-  a.n_ntiles = static_cast<int>((N + 255) / 256);
+  a.n_ntiles = static_cast<int>((N + 256 * NB - 1) / (256 * NB));
   a.out = Y;
   a.ldo = ldy;
   a.residual = static_cast<const __nv_bfloat16*>(residual);
-  return w_kmajor ? launch_pair<false>(a, st) : launch_pair<true>(a, st);
+  a.debug = g_debug_flags;
+  if (NB == 2) return w_kmajor ? launch_pair<false, 2>(a, st) : launch_pair<true, 2>(a, st);
+  return w_kmajor ? launch_pair<false, 1>(a, st) : launch_pair<true, 1>(a, st);
 }
 
 // Base GEMM (+ fused LoRA expand).  A: [M][K] K-major.  W: see w_kmajor.
