@@ -220,8 +220,11 @@ def main() -> None:
     # ---------------------------------------------------------------- timed region (device)
     timer = ops.KernelTimer()
     launches0 = ops.launch_count()
+    profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
     with ClockSampler(local) as clocks:
         barrier()
+        if profile_range:
+            torch.cuda.profiler.start()
         ops.set_timer(timer)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -231,6 +234,8 @@ def main() -> None:
         e1.record()
         ops.set_timer(None)
         barrier()
+        if profile_range:
+            torch.cuda.profiler.stop()
     launches = ops.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     kstats = timer.summary()
