@@ -1,0 +1,130 @@
+"""Planner drop-in (paper_2508_02932_b200.sweep) vs the reference planner.
+
+1. The reference's OWN test files for the planner side (test_planner, test_packing,
+   test_costmodel, test_workload, test_simulator, acceptance crit. 3-9) run against
+   this implementation through a module alias (tests/_lorasweep_alias.py).
+2. Cross-implementation parity: identical serialize_queue documents (byte for byte)
+   and identical solve_subproblem selections on seeded random instances.
+Both need /root/reference (present in the build container, absent on GPU boxes).
+"""
+
+import importlib
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+REF = Path("/root/reference/pkg")
+ROOT = Path(__file__).resolve().parent.parent
+needs_ref = pytest.mark.skipif(not REF.exists(), reason="reference checkout not present")
+
+
+@needs_ref
+def test_reference_planner_suite_passes_against_this_implementation():
+    files = [str(REF / "tests" / f) for f in ("test_planner.py", "test_packing.py", "test_costmodel.py",
+                                              "test_workload.py", "test_simulator.py", "test_acceptance.py")]
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1",
+               PYTHONPATH=f"{ROOT}:{ROOT / 'tests'}:{env_path() if (env_path := os.environ.get('PYTHONPATH')) else ''}")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-p", "_lorasweep_alias", "-p", "no:cacheprovider", "-q",
+                        "-k", "not criterion_1 and not criterion_2", *files], cwd="/tmp", env=env,
+                       capture_output=True, text=True, timeout=900)
+    tail = r.stdout[-3000:]
+    assert r.returncode == 0, tail
+    assert " passed" in tail and "failed" not in tail
+
+
+def _load_reference():
+    sys.path.insert(0, str(REF / "src"))
+    sys.path.insert(0, str(REF / "tests"))
+    try:
+        ref = importlib.import_module("lorasweep")
+        support = importlib.import_module("support")
+    finally:
+        sys.path.pop(0)
+        sys.path.pop(0)
+    return ref, support
+
+
+def _convert(obj, mod):
+    """Rebuild a reference value object with this repo's classes (same fields)."""
+    from dataclasses import fields, is_dataclass
+    if is_dataclass(obj) and not isinstance(obj, type):
+        cls = getattr(mod, type(obj).__name__)
+        return cls(**{f.name: _convert(getattr(obj, f.name), mod) for f in fields(obj)})
+    if isinstance(obj, tuple):
+        return tuple(_convert(x, mod) for x in obj)
+    if isinstance(obj, list):
+        return [_convert(x, mod) for x in obj]
+    return obj
+
+
+@needs_ref
+def test_queues_byte_identical_to_reference():
+    ref, support = _load_reference()
+    from paper_2508_02932_b200 import sweep as S
+    rng = np.random.default_rng(2024)
+    checked = 0
+    for _ in range(40):
+        gpus, configs, tm, mem, pool = support.random_planner_instance(rng)
+        q_ref = ref.serialize_queue(ref.plan_jobs(gpus, configs, tm, mem, workload_digest="d"))
+        my_configs = [_convert(c, S) for c in configs]
+        my_tm = S.TimeModel(coeffs=dict(tm.coeffs), load_scale=tm.load_scale)
+        my_mem = S.MemoryContext(_convert(mem.model, S), _convert(pool, S), my_configs)
+        q_me = S.serialize_queue(S.plan_jobs(gpus, my_configs, my_tm, my_mem, workload_digest="d"))
+        assert q_me == q_ref
+        checked += 1
+    assert checked == 40
+    # multi-batch and the 120-config sweep-shaped instances (8 GPUs, large knapsacks)
+    for builder, seed in ((support.multi_batch_instance, 3), (support.sweep_shaped_instance, 5)):
+        gpus, configs, tm, mem, pool = builder(np.random.default_rng(seed))
+        q_ref = ref.serialize_queue(ref.plan_jobs(gpus, configs, tm, mem))
+        my_configs = [_convert(c, S) for c in configs]
+        my_mem = S.MemoryContext(_convert(mem.model, S), _convert(pool, S), my_configs)
+        q_me = S.serialize_queue(S.plan_jobs(gpus, my_configs, S.TimeModel(coeffs=dict(tm.coeffs)), my_mem))
+        assert q_me == q_ref
+
+
+@needs_ref
+def test_subproblem_selection_identical_to_reference():
+    ref, support = _load_reference()
+    from paper_2508_02932_b200 import sweep as S
+    rng = np.random.default_rng(99)
+    for _ in range(200):
+        degree, configs, tm, mem = support.random_subproblem_instance(rng)
+        my_configs = [_convert(c, S) for c in configs]
+        my_tm = S.TimeModel(coeffs=dict(tm.coeffs), load_scale=tm.load_scale)
+        my_mem = S.MemoryContext(_convert(mem.model, S), _convert(mem.pool, S), my_configs)
+        try:
+            a = ref.solve_subproblem(degree, configs, tm, mem)
+        except ref.NoFeasiblePacking:
+            with pytest.raises(S.NoFeasiblePacking):
+                S.solve_subproblem(degree, my_configs, my_tm, my_mem)
+            continue
+        b = S.solve_subproblem(degree, my_configs, my_tm, my_mem)
+        assert (a.selected, a.degree, a.throughput, a.memory_used) == (b.selected, b.degree, b.throughput,
+                                                                       b.memory_used)
+
+
+def test_place_lowest_free_index_and_no_overlap():
+    from paper_2508_02932_b200 import sweep as S
+    model = S.ModelSpec("m", 1, (S.TargetModule("q", 1 << 20, 1 << 20),), 0, 2)
+    configs = [S.LoraConfig(f"c{i}", rank=8, alpha=16.0, batch_size=1, learning_rate=1e-4, seq_len=1,
+                            train_steps=1 + i % 3) for i in range(12)]
+    per = S.lora_state_memory(configs[0], model, S.ShardingSpec()).total_bytes
+    pool = S.GpuPool(8, int(per * 2.5))
+    tm = S.TimeModel(coeffs={1: (1.0, 1e-7), 2: (0.6, 1e-7), 4: (0.4, 1e-7), 8: (0.3, 1e-7)})
+    mem = S.MemoryContext(model, pool, configs)
+    q = S.plan_jobs(8, configs, tm, mem)
+    pl = S.place(q, 8)
+    assert set(pl.devices) == {j.id for j in q.jobs()}
+    jobs = q.jobs()
+    for a in jobs:
+        assert len(pl.devices[a.id]) == a.degree and all(0 <= d < 8 for d in pl.devices[a.id])
+        for b in jobs:
+            if a.id < b.id and set(pl.devices[a.id]) & set(pl.devices[b.id]):
+                assert pl.end_s[a.id] <= pl.start_s[b.id] or pl.end_s[b.id] <= pl.start_s[a.id]
+    first = q.batches[0].policy.jobs[0]
+    assert pl.devices[first.id] == tuple(range(first.degree))
