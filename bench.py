@@ -275,8 +275,13 @@ def main() -> None:
         except Exception:
             traffic = None
     kernels = {}
+    shapes = {}
     for kind, d in kstats.items():
         sec = d["ms"] / 1000.0
+        if "[" in kind:   # per-shape GEMM detail
+            shapes[kind[kind.index("[") + 1:-1]] = {"launches": d["launches"], "ms": round(d["ms"], 2),
+                                                   "tflops": round(d["flops"] / sec / 1e12, 1)}
+            continue
         kernels[kind] = {"launches": d["launches"], "ms_total": round(d["ms"], 3),
                          "share_of_step": round(d["ms"] / ms, 4)}
         if d["flops"]:
@@ -300,6 +305,7 @@ def main() -> None:
                      "step_base_gemm_tflops": round(base_tf, 1),
                      "step_frac_of_burst_peak": round(base_tf / peaks["tflops_burst"], 4)},
         "kernels": kernels,
+        "gemm_shapes": shapes,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": tokens_host.numel() * tokens_host.element_size(),
                 "d2h_bytes_per_step": losses_host.numel() * losses_host.element_size()},
         "gpu_launches": launches,

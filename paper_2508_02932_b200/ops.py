@@ -35,12 +35,15 @@ class KernelTimer:
         e.record()
         return e
 
-    def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0):
+    def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0, detail: str | None = None):
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         self.records.append((kind, e0, e1, flops, nbytes))
+        if detail is not None:
+            self.records.append((f"{kind}[{detail}]", e0, e1, flops, nbytes))
 
     def summary(self) -> dict:
+        """Per kernel class (and per GEMM shape, keys 'gemm[N..K..]'): launches, ms, flops, bytes."""
         torch.cuda.synchronize()
         out: dict = {}
         for kind, e0, e1, fl, nb in self.records:
@@ -102,7 +105,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, w_kmajor: bool = True, out: torch.Ten
         out.stride(0), _need(residual, "residual", allow_none=True)), "plora_gemm_bf16")
     _LAUNCHES[0] += 1
     if t is not None:
-        _TIMER.stop("gemm", t, flops=2.0 * M * N * K)
+        _TIMER.stop("gemm", t, flops=2.0 * M * N * K, detail=f"N{N}K{K}{'k' if w_kmajor else 'mn'}")
     return out
 
 
@@ -174,7 +177,7 @@ def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bo
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)
-        _TIMER.stop("gemm", t, flops=2.0 * T * d * k + 2.0 * k * tr)
+        _TIMER.stop("gemm", t, flops=2.0 * T * d * k + 2.0 * k * tr, detail=f"N{k}K{d}{'k' if w_kmajor else 'mn'}")
     return y_out
 
 
