@@ -389,7 +389,10 @@ struct PairCfg {
   static constexpr int kStages = NB == 1 ? 6 : 4;
   static constexpr int kAccStages = NB == 1 ? 2 : 1;
   static constexpr int kTmemCols = 512;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;      // producer + MMA + epilogue
+  static constexpr int kStgBytes = kEpiWarps * 32 * 32 * 4; // per warp: 32 rows x 32 fp32 (XOR-swizzled)
+  static constexpr int kSmemBytes = kStages * kStageBytes + 256 + kStgBytes + 1024;
   static constexpr int kBand = 8;                           // pair tiles per raster band
 };
 
@@ -432,7 +435,7 @@ __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx)
 __device__ __forceinline__ uint32_t peer_masked(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
 
 template <bool B_MN, int NB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
     plora_gemm_pair_kernel(const __grid_constant__ GemmArgs args) {
   using Cfg = PairCfg<NB>;
   constexpr int S = Cfg::kStages;
@@ -466,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&tempty_bar[s], 2 * Cfg::kEpiWarps);  // epilogue warps of both CTAs (leader's copy)
     }
     fence_mbar_init();
   }
@@ -568,66 +571,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
+    // 8 warps: warp w drains TMEM lane quarter w%4, column half (w-2)/4.  Per 32-column
+    // chunk: TMEM -> registers (thread = row) -> per-warp smem staging (fp32, XOR-swizzled
+    // 16-byte slots) -> coalesced global stores (4 lanes per 64-byte row segment, 8 rows
+    // per instruction).  The residual for the next chunk is prefetched while the current
+    // one is converted, hiding its global-load latency.
+    const int ew = warp - 2;
+    const int quarter = warp & 3;         // tcgen05.ld lane-quarter rule: warp w reads lanes 32*(w%4)..
+    const int chalf = ew >> 2;
+    constexpr int kChunks = Cfg::kBN / 32 / 2;   // chunks per warp
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    float4* stg = reinterpret_cast<float4*>(smem + S * Cfg::kStageBytes + 256) + ew * 32 * 8;
+    const int sub_r = lane >> 2;          // row within an 8-row pass
+    const int sub_q = (lane & 3) * 2;     // first of two 16-byte slots (8 columns)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int idx = cluster; idx < total; idx += n_clusters) {
       const PairTile t = decode_pair_tile<NB>(args, idx);
-      const int m0 = t.m0 + static_cast<int>(rank) * 128;
-      const int m_len = min(128, t.m_len - static_cast<int>(rank) * 128);
+      const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;   // this warp's 32 rows
+      const int m_len = min(32, t.m_len - static_cast<int>(rank) * 128 - quarter * 32);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
-      const bool row_ok = row < m_len;
-      const int64_t orow = static_cast<int64_t>(m0 + row) * args.ldo;
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow;
-      const __nv_bfloat16* res = args.residual ? args.residual + orow : nullptr;
+      const int c0 = chalf * kChunks;
+      uint4 res_next[4];
+      auto load_res = [&](int c, uint4 (&dst)[4]) {
+        const int col = t.n0 + c * 32 + sub_q * 4;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int rr = p * 8 + sub_r;
+          dst[p] = make_uint4(0, 0, 0, 0);
+          if (args.residual && rr < m_len && col < args.N)
+            dst[p] = *reinterpret_cast<const uint4*>(args.residual + static_cast<int64_t>(m0 + rr) * args.ldo + col);
+        }
+      };
+      if (!(args.debug & 1)) load_res(c0, res_next);
 #pragma unroll 1
-      for (int c = 0; c < ((args.debug & 1) ? 0 : Cfg::kBN / 32); ++c) {
+      for (int c = c0; c < ((args.debug & 1) ? c0 : c0 + kChunks); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tb + c * 32, r);
+        uint4 res[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) res[p] = res_next[p];
+        if (c + 1 < c0 + kChunks) load_res(c + 1, res_next);
         tmem_ld_wait();
-        const int col0 = t.n0 + c * 32;
-        if (row_ok && col0 < args.N) {
-          float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (col0 + 32 <= args.N) {
-            if (res) {
+        for (int q = 0; q < 8; ++q)
+          stg[lane * 8 + (q ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        __syncwarp();
+        const int col = t.n0 + c * 32 + sub_q * 4;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint4 rv = *reinterpret_cast<const uint4*>(res + col0 + q * 8);
-                const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+        for (int p = 0; p < 4; ++p) {
+          const int rr = p * 8 + sub_r;
+          if (rr < m_len && col < args.N) {
+            const float4 a = stg[rr * 8 + (sub_q ^ (rr & 7))];
+            const float4 b = stg[rr * 8 + ((sub_q + 1) ^ (rr & 7))];
+            float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            if (args.residual) {
+              const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&res[p]);
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  const float2 f = __bfloat1622float2(rh[h]);
-                  v[q * 8 + 2 * h] += f.x;
-                  v[q * 8 + 2 * h + 1] += f.y;
-                }
+              for (int h = 0; h < 4; ++h) {
+                const float2 f = __bfloat1622float2(rh[h]);
+                v[2 * h] += f.x;
+                v[2 * h + 1] += f.y;
               }
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-              w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-              w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-              w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-              *reinterpret_cast<uint4*>(o + col0 + q * 8) = w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (col0 + j < args.N) {
-                float x = v[j];
-                if (res) x += __bfloat162float(res[col0 + j]);
-                o[col0 + j] = __float2bfloat16_rn(x);
-              }
-            }
+            uint4 w;
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                      static_cast<int64_t>(m0 + rr) * args.ldo + col) = w;
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();

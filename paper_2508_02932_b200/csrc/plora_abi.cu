@@ -154,7 +154,7 @@ static int launch_pair(const GemmArgs& args, cudaStream_t stream) {
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
   const int clusters = total < max_clusters ? total : max_clusters;
-  kern<<<clusters * 2, kThreads, PairCfg<NB>::kSmemBytes, stream>>>(args);
+  kern<<<clusters * 2, PairCfg<NB>::kThreads, PairCfg<NB>::kSmemBytes, stream>>>(args);
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
