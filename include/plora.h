@@ -105,7 +105,8 @@ PLORA_API int plora_gemm_bf16(void* stream, int64_t M, int64_t N, int64_t K,
  *   Hs = alpha_i * X_i A_i                         (K2a shrink, tcgen05)
  *   Y  = X op(W) + Hs_i B_i (+ residual)           (K1 GEMM, K2b as extra K-steps)
  * X bf16 [T][d]; W bf16 [k][d] (w_kmajor=1) or [d][k] (w_kmajor=0);
- * A_sh, Bt_sh as above; Hs_out bf16 [T][rpad64]; Y bf16 [T][ldy]. */
+ * A_sh, Bt_sh as above; Hs_out bf16 [T][rpad64]; Y bf16 [T][ldy].
+ * residual (may be NULL; may equal Y for in-place accumulation): Y = result + residual. */
 PLORA_API int plora_linear_fwd(void* stream, const plora_pack_t* pack,
                      const void* X, int64_t d, int64_t k,
                      const void* W, int32_t w_kmajor,
@@ -166,6 +167,9 @@ PLORA_API int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks,
  * and stores rstd[rows]; 1 recomputes y from a saved rstd).  bf16 [rows][d], d <= 8192. */
 PLORA_API int plora_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const void* x, const void* w,
                                 float eps, void* y, float* rstd, int32_t use_given_rstd);
+/* Fused residual add + RMSNorm: sum = a + b (bf16), y = rmsnorm(sum) * w, rstd[rows]. */
+PLORA_API int plora_add_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const void* a, const void* b,
+                                    const void* w, float eps, void* sum, void* y, float* rstd);
 /* dx = rstd * (g - xhat * mean(g * xhat)) (+ residual), g = dy * w. */
 PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const void* dy, const void* x,
                                 const float* rstd, const void* w, const void* residual, void* dx);

@@ -29,6 +29,7 @@ EXPORTS = (
     "plora_linear_bwd",
     "plora_adamw",
     "plora_rmsnorm_fwd",
+    "plora_add_rmsnorm_fwd",
     "plora_rmsnorm_bwd",
     "plora_swiglu_fwd",
     "plora_swiglu_bwd",
@@ -92,6 +93,7 @@ _SIGNATURES = {
     "plora_adamw": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _i64],
                     ctypes.c_int),
     "plora_rmsnorm_fwd": ([_vp, _i64, _i64, _vp, _vp, _f32, _vp, _vp, _i32], ctypes.c_int),
+    "plora_add_rmsnorm_fwd": ([_vp, _i64, _i64, _vp, _vp, _vp, _f32, _vp, _vp, _vp], ctypes.c_int),
     "plora_rmsnorm_bwd": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "plora_swiglu_fwd": ([_vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_swiglu_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),

@@ -96,6 +96,47 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(const bf16* _
   }
 }
 
+// Fused residual add + RMSNorm: s = a + b (written to sum), y = s * rstd * w.
+__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(const bf16* __restrict__ a,
+                                                                   const bf16* __restrict__ b,
+                                                                   const bf16* __restrict__ w,
+                                                                   bf16* __restrict__ sum, bf16* __restrict__ y,
+                                                                   float* __restrict__ rstd, int d, float eps) {
+  __shared__ float red[kNormThreads / 32];
+  const int64_t row = blockIdx.x;
+  float v[kMaxV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kMaxV; ++j) {
+    const int c = (j * kNormThreads + threadIdx.x) * 8;
+    if (c < d) {
+      float bf[8];
+      load8(a + row * d + c, v[j]);
+      load8(b + row * d + c, bf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)   // normalise the bf16-rounded sum (what the backward sees)
+        v[j][e] = __bfloat162float(__float2bfloat16_rn(v[j][e] + bf[e]));
+      store8(sum + row * d + c, v[j]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += v[j][e] * v[j][e];
+    }
+  }
+  ss = block_sum<kNormThreads>(ss, red);
+  const float r = rsqrtf(ss / d + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+#pragma unroll
+  for (int j = 0; j < kMaxV; ++j) {
+    const int c = (j * kNormThreads + threadIdx.x) * 8;
+    if (c < d) {
+      float wf[8], o[8];
+      load8(w + c, wf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = v[j][e] * r * wf[e];
+      store8(y + row * d + c, o);
+    }
+  }
+}
+
 // dx = rstd * (g - xhat * mean(g * xhat)) (+ residual), g = dy * w, xhat = x * rstd.
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* __restrict__ dy,
                                                                    const bf16* __restrict__ x,
@@ -315,6 +356,16 @@ PLORA_API int plora_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const voi
       static_cast<const bf16*>(x), static_cast<const bf16*>(w), static_cast<bf16*>(y), rstd, (int)d, eps,
       use_given_rstd);
   return launch_status("rmsnorm_fwd");
+}
+
+PLORA_API int plora_add_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const void* a, const void* b,
+                                    const void* w, float eps, void* sum, void* y, float* rstd) {
+  if (d % 8 || d > 8 * kNormThreads * kMaxV) return plora::set_error("rmsnorm: d must be a multiple of 8, <= 8192");
+  if (rows <= 0) return 0;
+  add_rmsnorm_kernel<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(a), static_cast<const bf16*>(b), static_cast<const bf16*>(w), static_cast<bf16*>(sum),
+      static_cast<bf16*>(y), rstd, (int)d, eps);
+  return launch_status("add_rmsnorm_fwd");
 }
 
 PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const void* dy, const void* x,

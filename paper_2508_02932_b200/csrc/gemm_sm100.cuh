@@ -31,6 +31,7 @@ struct __align__(64) GemmArgs {
   CUtensorMap tmB;  // main B operand
   CUtensorMap tmH;  // LoRA-block A operand: Hs or dH, K-major [T][64nb]
   CUtensorMap tmL;  // LoRA-block B operand: 3D [n][N][64nb], K-major
+  CUtensorMap tmY;  // output [M][N] bf16, 32x32 boxes, SWIZZLE_64B (pair-kernel TMA store epilogue)
   const int32_t* mtiles;    // GEMM/SHRINK tile list [n_groups][4]; nullptr = uniform 128-row tiles
   const int64_t* row_off;   // SEGRED: token segment offsets [n+1]
   const int32_t* ranks;     // GEMM with LoRA: r_i
@@ -48,6 +49,7 @@ struct __align__(64) GemmArgs {
   int32_t has_lora;
   int32_t nb;        // 64-column rank blocks
   int32_t debug;     // bit 0: skip epilogue stores (profiling experiments only)
+  int32_t accumulate;  // pair kernel: Y += result (TMA reduce-add) instead of Y = result
 };
 
 constexpr int kBM = 128;
@@ -391,8 +393,8 @@ struct PairCfg {
   static constexpr int kTmemCols = 512;
   static constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;      // producer + MMA + epilogue
-  static constexpr int kStgBytes = kEpiWarps * 32 * 32 * 4; // per warp: 32 rows x 32 fp32 (XOR-swizzled)
-  static constexpr int kSmemBytes = kStages * kStageBytes + 256 + kStgBytes + 1024;
+  static constexpr int kStgBytes = kEpiWarps * 2 * 2048;   // per warp: 2 x [32 rows x 32 bf16], SW64
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*barriers*/ + kStgBytes + 1024 /*align*/;
   static constexpr int kBand = 8;                           // pair tiles per raster band
 };
 
@@ -571,21 +573,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    // 8 warps: warp w drains TMEM lane quarter w%4, column half (w-2)/4.  Per 32-column
-    // chunk: TMEM -> registers (thread = row) -> per-warp smem staging (fp32, XOR-swizzled
-    // 16-byte slots) -> coalesced global stores (4 lanes per 64-byte row segment, 8 rows
-    // per instruction).  The residual for the next chunk is prefetched while the current
-    // one is converted, hiding its global-load latency.
+    // 8 warps: warp w drains TMEM lane quarter w%4, column half (w-2)/4, in 32-column
+    // chunks: TMEM -> registers (thread = row) -> bf16 -> per-warp smem staging (two
+    // 2 KB buffers, 64-byte swizzle, bank-conflict free) -> TMA bulk tensor store, or
+    // TMA reduce-add when accumulating into Y.  Stores are asynchronous, so TMEM is
+    // released as soon as the last chunk is in registers.  Warps whose 32 rows are only
+    // partly inside the tile (unaligned segments) fall back to masked direct stores.
     const int ew = warp - 2;
     const int quarter = warp & 3;         // tcgen05.ld lane-quarter rule: warp w reads lanes 32*(w%4)..
     const int chalf = ew >> 2;
     constexpr int kChunks = Cfg::kBN / 32 / 2;   // chunks per warp
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
-    float4* stg = reinterpret_cast<float4*>(smem + S * Cfg::kStageBytes + 256) + ew * 32 * 8;
-    const int sub_r = lane >> 2;          // row within an 8-row pass
-    const int sub_q = (lane & 3) * 2;     // first of two 16-byte slots (8 columns)
+    uint8_t* stg = smem + S * Cfg::kStageBytes + 1024 + ew * 4096;   // 1024-B aligned (>= swizzle period)
     int acc = 0;
     uint32_t acc_phase = 0;
+    int issued = 0;
     for (int idx = cluster; idx < total; idx += n_clusters) {
       const PairTile t = decode_pair_tile<NB>(args, idx);
       const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;   // this warp's 32 rows
@@ -594,65 +596,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
       const int c0 = chalf * kChunks;
-      uint4 res_next[4];
-      auto load_res = [&](int c, uint4 (&dst)[4]) {
-        const int col = t.n0 + c * 32 + sub_q * 4;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const int rr = p * 8 + sub_r;
-          dst[p] = make_uint4(0, 0, 0, 0);
-          if (args.residual && rr < m_len && col < args.N)
-            dst[p] = *reinterpret_cast<const uint4*>(args.residual + static_cast<int64_t>(m0 + rr) * args.ldo + col);
-        }
-      };
-      if (!(args.debug & 1)) load_res(c0, res_next);
+      const bool skip = (args.debug & 1) != 0;
+      uint32_t r[32];
+      if (!skip) tmem_ld_32x32b_x32(tb + c0 * 32, r);
 #pragma unroll 1
-      for (int c = c0; c < ((args.debug & 1) ? c0 : c0 + kChunks); ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tb + c * 32, r);
-        uint4 res[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) res[p] = res_next[p];
-        if (c + 1 < c0 + kChunks) load_res(c + 1, res_next);
+      for (int j = 0; j < (skip ? 0 : kChunks); ++j) {
+        const int c = c0 + j;
         tmem_ld_wait();
+        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          stg[lane * 8 + (q ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-        __syncwarp();
-        const int col = t.n0 + c * 32 + sub_q * 4;
+        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+        if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c + 1) * 32, r);   // overlaps the stores below
+        const int col0 = t.n0 + c * 32;
+        if (col0 >= args.N || m_len <= 0 || (args.debug & 4)) continue;   // bit 2: TMEM drain only (experiment)
+        if (m_len == 32) {
+          uint8_t* buf = stg + (j & 1) * 2048;
+          if (issued >= 2) {
+            if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has read it
+            __syncwarp();
+          }
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const int rr = p * 8 + sub_r;
-          if (rr < m_len && col < args.N) {
-            const float4 a = stg[rr * 8 + (sub_q ^ (rr & 7))];
-            const float4 b = stg[rr * 8 + ((sub_q + 1) ^ (rr & 7))];
-            float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            if (args.residual) {
-              const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&res[p]);
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(buf + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (args.accumulate) tma_reduce_add_2d(&args.tmY, buf, col0, m0);
+            else                 tma_store_2d(&args.tmY, buf, col0, m0);
+            bulk_commit();
+          }
+          ++issued;
+        } else if (lane < m_len) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(m0 + lane) * args.ldo;
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(pk);
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float2 f = __bfloat1622float2(rh[h]);
-                v[2 * h] += f.x;
-                v[2 * h + 1] += f.y;
+          for (int q = 0; q < 16; ++q) {
+            const int cc = col0 + 2 * q;
+            if (cc < args.N) {
+              float2 f = __bfloat1622float2(h[q]);
+              if (args.accumulate) {
+                const float2 old = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + cc));
+                f.x += old.x;
+                f.y += old.y;
               }
+              *reinterpret_cast<__nv_bfloat162*>(o + cc) = __floats2bfloat162_rn(f.x, f.y);
             }
-            uint4 w;
-            w.x = pack_bf16x2(v[0], v[1]);
-            w.y = pack_bf16x2(v[2], v[3]);
-            w.z = pack_bf16x2(v[4], v[5]);
-            w.w = pack_bf16x2(v[6], v[7]);
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                      static_cast<int64_t>(m0 + rr) * args.ldo + col) = w;
           }
         }
-        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
       if (++acc == AS) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();   // all TMA stores complete before the CTA retires
+    __syncwarp();
   }
 
   tc_fence_before();

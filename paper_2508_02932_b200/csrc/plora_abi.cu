@@ -83,6 +83,23 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   return 0;
 }
 
+// 2D bf16 output tensor for the TMA-store epilogue: 32x32 boxes, 64-byte swizzle.
+static int make_map_out(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_elems) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if (reinterpret_cast<uintptr_t>(base) % 16 || (pitch_elems * 2) % 16)
+    return fail("output base/pitch not 16-byte aligned");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled(out) failed: %d", (int)r);
+  return 0;
+}
+
 // 3D bf16 tensor [n][mid][inner] (dense), box {box_inner, box_mid, 1}.
 static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t mid, uint64_t n,
                        uint32_t box_inner, uint32_t box_mid) {
@@ -193,7 +210,14 @@ static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, i
   a.n_ntiles = static_cast<int>((N + 256 * NB - 1) / (256 * NB));
   a.out = Y;
   a.ldo = ldy;
-  a.residual = static_cast<const __nv_bfloat16*>(residual);
+  if ((rc = make_map_out(&a.tmY, Y, N, M, ldy))) return rc;
+  // Y = result + residual is computed as Y <- residual (skipped when in place), then a
+  // TMA reduce-add of the result (bf16 add in L2).
+  if (residual) {
+    if (residual != Y)
+      PLORA_CUDA(cudaMemcpy2DAsync(Y, ldy * 2, residual, ldy * 2, N * 2, M, cudaMemcpyDeviceToDevice, st));
+    a.accumulate = 1;
+  }
   a.debug = g_debug_flags;
   if (NB == 2) return w_kmajor ? launch_pair<false, 2>(a, st) : launch_pair<true, 2>(a, st);
   return w_kmajor ? launch_pair<false, 1>(a, st) : launch_pair<true, 1>(a, st);

@@ -26,6 +26,19 @@ def rmsnorm_fwd(x: torch.Tensor, w: torch.Tensor, eps: float):
     return y, rstd
 
 
+def add_rmsnorm_fwd(a: torch.Tensor, b: torch.Tensor, w: torch.Tensor, eps: float):
+    """(sum = a + b, rmsnorm(sum) * w, rstd): the residual add fused into the norm."""
+    rows, d = a.shape
+    s_ = torch.empty_like(a)
+    y = torch.empty_like(a)
+    rstd = torch.empty(rows, dtype=torch.float32, device=a.device)
+    _lib.check(_lib.lib().plora_add_rmsnorm_fwd(_stream(), rows, d, _need(a, "a"), _need(b, "b"), _need(w, "w"), eps,
+                                                _need(s_, "sum"), _need(y, "y"), _need(rstd, "rstd", torch.float32)),
+               "add_rmsnorm_fwd")
+    _LAUNCHES[0] += 1
+    return s_, y, rstd
+
+
 def rmsnorm_apply(x: torch.Tensor, rstd: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None):
     rows, d = x.shape
     y = torch.empty_like(x) if out is None else out

@@ -233,11 +233,19 @@ class PackedLoraTrainer:
                               dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
 
     # ------------------------------------------------------------------ forward
-    def _layer_fwd(self, layer: int, h: torch.Tensor) -> tuple[torch.Tensor, _LayerSave]:
+    def _layer_fwd(self, layer: int, h_prev: torch.Tensor, delta: torch.Tensor | None
+                   ) -> tuple[torch.Tensor, torch.Tensor, _LayerSave]:
+        """h = h_prev + delta (the previous layer's down-projection output, added inside
+        the fused add+RMSNorm); returns (h_mid, down_out) -- this layer's output is their
+        sum, materialised by the next layer's (or the final) add+RMSNorm."""
         cfg, lw = self.cfg, self.base.layers[layer]
         T, hd, H, KV, s = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv, self.s
         B = T // s
-        x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
+        if delta is None:
+            h = h_prev
+            x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
+        else:
+            h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
         q, hs_q = self._lin_fwd(layer, "q", x1, lw["q"])
         k, hs_k = self._lin_fwd(layer, "k", x1, lw["k"])
         v, hs_v = self._lin_fwd(layer, "v", x1, lw["v"])
@@ -254,17 +262,18 @@ class PackedLoraTrainer:
         with torch.enable_grad():
             og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
         attn = ew.rope(og.detach().transpose(1, 2), self.cos, self.sin, s, rotate=False)   # [T][H*hd]
-        h_mid, hs_o = self._lin_fwd(layer, "o", attn, lw["o"], residual=h)
-        x2, rstd2 = ew.rmsnorm_fwd(h_mid, lw["mlp_norm"], cfg.norm_eps)
+        o_out, hs_o = self._lin_fwd(layer, "o", attn, lw["o"])
+        h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
+        del o_out
         g, hs_g = self._lin_fwd(layer, "gate", x2, lw["gate"])
         u, hs_u = self._lin_fwd(layer, "up", x2, lw["up"])
         del x2
         act = ew.swiglu_fwd(g, u)
-        h_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"], residual=h_mid)
+        d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
                           attn_out=attn, g=g, u=u,
                           hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d})
-        return h_out, save
+        return h_mid, d_out, save
 
     # ------------------------------------------------------------------ backward
     def _layer_bwd(self, layer: int, sv: _LayerSave, dh: torch.Tensor, need_dx: bool) -> torch.Tensor:
@@ -300,11 +309,11 @@ class PackedLoraTrainer:
         return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid, out=dx1)
 
     # ------------------------------------------------------------------ loss head
-    def _head(self, h: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
-        """Final norm + lm_head + per-adapter-mean CE, chunked over tokens; returns d h.
-        Writes per-adapter losses into self.losses."""
+    def _head(self, h_prev: torch.Tensor, delta: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
+        """Final (add+)norm + lm_head + per-adapter-mean CE, chunked over tokens; returns
+        d h.  Writes per-adapter losses into self.losses."""
         cfg = self.cfg
-        xf, rstd = ew.rmsnorm_fwd(h, self.base.final_norm, cfg.norm_eps)
+        h, xf, rstd = ew.add_rmsnorm_fwd(h_prev, delta, self.base.final_norm, cfg.norm_eps)
         dxf = torch.empty_like(xf)
         labels = torch.roll(tokens, -1)
         tok_loss = torch.empty(self.T, dtype=torch.float32, device=self.device)
@@ -325,12 +334,13 @@ class PackedLoraTrainer:
     def forward_backward(self, tokens: torch.Tensor) -> torch.Tensor:
         """Full packed forward + backward; fills bank.G; returns per-adapter losses (device)."""
         h = self.base.embed[tokens]
+        delta = None
         saves = []
         for layer in range(self.cfg.n_layers):
-            h, sv = self._layer_fwd(layer, h)
+            h, delta, sv = self._layer_fwd(layer, h, delta)
             saves.append(sv)
-        dh = self._head(h, tokens)
-        del h
+        dh = self._head(h, delta, tokens)
+        del h, delta
         for layer in reversed(range(self.cfg.n_layers)):
             sv = saves.pop()
             dh = self._layer_bwd(layer, sv, dh, need_dx=layer > 0)

@@ -30,6 +30,17 @@ def test_rmsnorm(d):
     assert torch.equal(inplace, ew.rmsnorm_bwd(dy, x, r, w, res))
 
 
+def test_add_rmsnorm():
+    a = (torch.randn(257, 4096, device="cuda") * 2).to(bf)
+    b = torch.randn(257, 4096, device="cuda").to(bf)
+    w = (torch.rand(4096, device="cuda") + 0.5).to(bf)
+    s_, y, r = ew.add_rmsnorm_fwd(a, b, w, 1e-5)
+    ref_s = (a.float() + b.float()).to(bf)
+    assert torch.equal(s_, ref_s)
+    ry, rr = ew.ref_rmsnorm_fwd(ref_s, w, 1e-5)
+    assert rel(y, ry) < 4e-3 and torch.allclose(r, rr, rtol=1e-5)
+
+
 def test_swiglu():
     g = (torch.randn(1000, 1024, device="cuda") * 2).to(bf)
     u = torch.randn(1000, 1024, device="cuda").to(bf)
