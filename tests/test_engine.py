@@ -1,0 +1,88 @@
+"""Execution-engine host logic (planner placement -> per-rank job lists -> gathered
+records / makespan) under torch.distributed gloo, world size 2, on CPU.  The GPU
+job runner is replaced by a deterministic fake; tests/test_gpu_engine.py runs real jobs."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2508_02932_b200 import sweep as S
+from paper_2508_02932_b200.sweep.engine import execute, rank_schedule
+
+
+def _instance(n=10, G=4):
+    model = S.ModelSpec("m", 1, (S.TargetModule("q", 1 << 20, 1 << 20),), 0, 2)
+    configs = [S.LoraConfig(f"c{i:02d}", rank=8 * (1 + i % 3), alpha=16.0, batch_size=1 + i % 2,
+                            learning_rate=1e-4, seq_len=16, train_steps=2 + i % 3) for i in range(n)]
+    per = S.lora_state_memory(configs[0], model, S.ShardingSpec()).total_bytes
+    pool = S.GpuPool(G, int(per * 4.5))
+    tm = S.TimeModel(coeffs={1: (1.0, 1e-4), 2: (1.0, 1e-4), 4: (1.0, 1e-4)})   # no TP speedup -> degree 1
+    mem = S.MemoryContext(model, pool, configs)
+    return configs, S.plan_jobs(G, configs, tm, mem), tm
+
+
+def fake_run(job, by_id, dev):
+    steps = max(by_id[c].train_steps for c in job.configs)
+    it = 0.1 + 0.01 * len(job.configs)
+    return steps, steps * it, it, [1.0] * len(job.configs)
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def gather(obj):
+        res = [None] * world
+        dist.all_gather_object(res, obj)
+        return res
+
+    configs, queue, _ = _instance()
+    rep = execute(queue, configs, 4, rank=rank, world=world, run_job=fake_run, all_gather=gather)
+    out[rank] = (rep["makespan_s"], sorted((r.job_id, r.device) for r in rep["records"]), rep["busy_s"])
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_engine_two_ranks_gloo():
+    configs, queue, _ = _instance()
+    assert all(j.degree == 1 for j in queue.jobs())
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r0, r1 = out[0], out[1]
+    assert r0 == r1                                       # every rank sees the same gathered report
+    placement = S.place(queue, 4)
+    expect = sorted((j.id, placement.devices[j.id][0]) for j in queue.jobs())
+    assert r0[1] == expect                                 # each job ran once, on its placed device
+    busy = r0[2]
+    assert set(busy) == {0, 1, 2, 3}
+    assert r0[0] == pytest.approx(max(busy.values()))
+
+
+def test_rank_schedule_matches_placement_and_covers_queue():
+    configs, queue, _ = _instance(n=14, G=4)
+    pl = S.place(queue, 4)
+    seen = []
+    for dev in range(4):
+        sched = rank_schedule(queue, pl, dev)
+        starts = [pl.start_s[j.id] for j in sched]
+        assert starts == sorted(starts)
+        seen += [j.id for j in sched]
+    # a degree-d job appears in the schedule of each of its d devices
+    assert sorted(seen) == sorted(j.id for j in queue.jobs() for _ in range(j.degree))
+
+
+def test_profiles_calibrate_time_model():
+    configs, queue, _ = _instance()
+    rep = execute(queue, configs, 4, run_job=fake_run)
+    assert len(rep["profiles"]) == len(queue.jobs())
+    tm = S.calibrate_time_model(rep["profiles"] * 1 + [S.ProfileRecord(1, (8,), (1,), 16, 0.11)])
+    assert tm.has_degree(1)
