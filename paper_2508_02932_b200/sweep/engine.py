@@ -48,6 +48,19 @@ def rank_schedule(queue: JobQueue, placement: Placement, rank: int) -> list:
     return sorted(mine, key=lambda j: (placement.start_s[j.id], j.id))
 
 
+_BASE_CACHE: dict = {}
+
+
+def _base(model_name: str, device: str):
+    """Frozen base weights are shared by every job a process runs on a device."""
+    from ..model import PRESETS, BaseWeights
+
+    key = (model_name, device)
+    if key not in _BASE_CACHE:
+        _BASE_CACHE[key] = BaseWeights(PRESETS[model_name], device)
+    return _BASE_CACHE[key]
+
+
 def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, steps_override: int | None = None,
                      warmup: int = 1) -> tuple:
     """Run one packed job on ``device``: returns (steps, seconds, mean iteration seconds, losses)."""
@@ -58,7 +71,7 @@ def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, ste
     cfgs = [configs_by_id[c] for c in job.configs]
     seq = max(c.seq_len for c in cfgs)
     specs = [AdapterSpec(rank=c.rank, alpha=c.alpha, batch=c.batch_size, lr=c.learning_rate) for c in cfgs]
-    trainer = PackedLoraTrainer(PRESETS[model_name], specs, seq, device=device,
+    trainer = PackedLoraTrainer(PRESETS[model_name], specs, seq, device=device, base=_base(model_name, device),
                                 adapter_seeds=[int(hashlib.sha256(c.id.encode()).hexdigest()[:8], 16) for c in cfgs])
     steps = steps_override or max(c.train_steps for c in cfgs)
     tokens = trainer.synthetic_tokens().to(device)

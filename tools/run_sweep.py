@@ -1,0 +1,117 @@
+"""C5: Llama-3.1-8B hyper-parameter sweep (64 configs) -- plan, place, execute, report.
+
+  python tools/run_sweep.py [--gpus 8] [--steps-measured 3] [--out gpurun_out/sweep.json]
+
+1. profile: a few packed jobs of different sizes run on cuda:0 -> ProfileRecords (degree 1);
+2. calibrate: TimeModel per the reference least-squares fit, with the B200 token term
+   (grid-searched token_weight; load = r*b*s + w*b*s) -- degrees > 1 are costed d x the
+   degree-1 job because tensor-parallel jobs are not built yet (so the planner uses degree 1);
+3. plan: plan_jobs on 8 x B200 (memory model from the Llama-3.1-8B shapes), Min-GPU /
+   Max-GPU baselines, predicted makespans (placement timeline == reference simulator rule);
+4. execute: the engine runs every job of the planned queue for --steps-measured steps on
+   its placed (virtual) device; with one physical GPU the 8 devices' jobs run back to
+   back and each device's busy time is measured separately (jobs share no data, so the
+   8-GPU makespan is the max over devices); step times are scaled to train_steps.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, ".")
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
+import numpy as np  # noqa: E402
+
+from paper_2508_02932_b200 import sweep as S  # noqa: E402
+from paper_2508_02932_b200.model import PRESETS  # noqa: E402
+from paper_2508_02932_b200.sweep.engine import execute, train_packed_job  # noqa: E402
+
+
+def grid(train_steps=50, seq=1024):
+    tmpl = S.LoraConfig("t", rank=8, alpha=16.0, batch_size=1, learning_rate=1e-4, seq_len=seq, train_steps=train_steps)
+    return S.enumerate_grid([5e-5, 1e-4, 2e-4, 4e-4], [1, 2], [8, 16, 32, 64], [16.0, 64.0], tmpl)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=8)
+    ap.add_argument("--steps-measured", type=int, default=3)
+    ap.add_argument("--mem-gb", type=float, default=178.0)
+    ap.add_argument("--out", default="gpurun_out/sweep.json")
+    args = ap.parse_args()
+    t_start = time.perf_counter()
+    cfg = PRESETS["llama-3.1-8b"]
+    configs = grid()
+    by_id = {c.id: c for c in configs}
+    # memory model: bf16 base; activations ~2.95 MB/token saved by the trainer (measured peak at T=32768)
+    model = S.model_spec_from_config(cfg, c_prec=2, act_coeffs=(0.0, 2.95e6 / 2 / 2, 2.95e6 / 2 / 2))
+    pool = S.GpuPool(args.gpus, int(args.mem_gb * 1e9), load_factor=0.9)
+
+    # 1. profile packs of 1 .. 16 configs at degree 1
+    rng = np.random.default_rng(0)
+    packs = [[0], [5, 17], list(range(0, 64, 16)), list(range(3, 64, 8)), list(rng.choice(64, 12, replace=False)),
+             list(range(1, 64, 4))]
+    profiles = []
+    for p in packs:
+        job = S.make_job([configs[i].id for i in p], 1, S.TimeModel(coeffs={1: (1.0, 0.0)}),
+                         S.MemoryContext(model, pool, configs))
+        steps, dt, it, _ = train_packed_job(job, by_id, "llama-3.1-8b", "cuda:0", steps_override=args.steps_measured)
+        cf = [by_id[c] for c in job.configs]
+        profiles.append(S.ProfileRecord(1, tuple(c.rank for c in cf), tuple(c.batch_size for c in cf), 1024, it))
+        print(f"profile: {len(p)} configs, {sum(c.batch_size for c in cf)} seqs -> {it:.3f} s/iter", flush=True)
+    best = None
+    for w in (0.0, 4.0, 16.0, 64.0, 256.0, 1024.0):
+        try:
+            tm1 = S.calibrate_time_model(profiles, token_weight=w, max_rel_rmse=1.0)
+        except S.CalibrationError:
+            continue
+        if best is None or tm1.fit_rel_rmse[1] < best.fit_rel_rmse[1]:
+            best = tm1
+    b1, m1 = best.params(1)
+    # degree d > 1 would need tensor parallelism (not built): cost it as d x the degree-1 job so the
+    # planner never prefers it (using d GPUs for the time of one)
+    tm = S.TimeModel(coeffs={d: (b1 * d, m1 * d) for d in (1, 2, 4, 8) if d <= args.gpus},
+                     token_weight=best.token_weight)
+    print(f"calibrated: base {b1:.4f} s, marginal {m1:.3e} s/load, token_weight {best.token_weight}, "
+          f"rel rmse {best.fit_rel_rmse[1]:.3f}", flush=True)
+
+    # 3. plan
+    mem = S.MemoryContext(model, pool, configs)
+    queue = S.plan_jobs(args.gpus, configs, tm, mem)
+    pl = S.place(queue, args.gpus)
+    qmin = S.min_gpu_queue(configs, args.gpus, tm, mem)
+    qmax = S.max_gpu_queue(configs, args.gpus, tm, mem)
+    pred = {"planned": pl.makespan, "min_gpu": S.place(qmin, args.gpus).makespan,
+            "max_gpu_no_tp_speedup": S.place(qmax, args.gpus).makespan}
+    print("predicted makespans (s):", {k: round(v, 1) for k, v in pred.items()}, flush=True)
+    print("jobs:", [(len(j.configs), j.degree) for j in queue.jobs()], flush=True)
+
+    # 4. execute (measured steps, scaled to train_steps)
+    rep = execute(queue, configs, args.gpus, steps_override=args.steps_measured)
+    scale = {r.job_id: max(by_id[c].train_steps for c in r.configs) for r in rep["records"]}
+    busy = {}
+    for r in rep["records"]:
+        busy[r.device] = busy.get(r.device, 0.0) + r.iter_time_s * scale[r.job_id]
+    measured = max(busy.values())
+    # min-GPU baseline measured the same way would run 64 single-config jobs; use its calibrated prediction
+    out = {"configs": len(configs), "gpus": args.gpus, "jobs": len(queue.jobs()),
+           "measured_makespan_s": measured, "measured_busy_s": busy,
+           "predicted_makespan_s": pred, "speedup_vs_min_gpu_pred": pred["min_gpu"] / measured,
+           "profiles": [dict(degree=p.parallelism_degree, ranks=list(p.packed_ranks), batch_sizes=list(p.packed_batch_sizes),
+                             seq_len=p.seq_len, iter_time_s=p.iter_time_s) for p in profiles + rep["profiles"]],
+           "time_model": {"base_s": b1, "marginal_s": m1, "token_weight": best.token_weight,
+                          "rel_rmse": best.fit_rel_rmse[1]},
+           "queue": json.loads(S.serialize_queue(queue)), "wall_s": time.perf_counter() - t_start,
+           "note": ("each job executed for --steps-measured steps on its placed device; with one physical GPU the "
+                    "8 devices' jobs run back to back and per-device busy time is summed separately")}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps({k: out[k] for k in ("jobs", "measured_makespan_s", "predicted_makespan_s",
+                                          "speedup_vs_min_gpu_pred", "wall_s")}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
