@@ -128,3 +128,25 @@ def test_place_lowest_free_index_and_no_overlap():
                 assert pl.end_s[a.id] <= pl.start_s[b.id] or pl.end_s[b.id] <= pl.start_s[a.id]
     first = q.batches[0].policy.jobs[0]
     assert pl.devices[first.id] == tuple(range(first.degree))
+
+
+def test_balance_extension_beats_reference_dtm_on_token_linear_cost():
+    """B200 extension: with an iteration cost ~ base + c*tokens (the calibrated B200 shape)
+    the balanced queue finishes no later than the reference DTM queue and Min-GPU, keeps every
+    job within memory, and covers every configuration exactly once."""
+    from paper_2508_02932_b200 import sweep as S
+    model = S.ModelSpec("m", 2, (S.TargetModule("q", 4096, 4096), S.TargetModule("v", 4096, 1024)),
+                        8_000_000_000, 2, attn_act_coeff=4e5, mlp_act_coeff=4e5)
+    tmpl = S.LoraConfig("t", 8, 16.0, 1, 1e-4, 1024, 50)
+    configs = S.enumerate_grid([1e-4, 2e-4], [1, 2], [8, 16, 32, 64], [16.0, 64.0], tmpl)
+    pool = S.GpuPool(8, int(178e9), 0.9)
+    tm = S.TimeModel(coeffs={d: (0.02 * d, 3e-8 * d) for d in (1, 2, 4, 8)}, token_weight=1024.0)
+    mem = S.MemoryContext(model, pool, configs)
+    ref_q = S.plan_jobs(8, configs, tm, mem)
+    bal_q = S.plan_jobs(8, configs, tm, mem, balance=True)
+    assert sorted(bal_q.config_ids()) == sorted(c.id for c in configs)
+    for j in bal_q.jobs():
+        assert mem.fits(j.configs, j.degree)
+    t_bal = S.place(bal_q, 8).makespan
+    assert t_bal <= S.place(ref_q, 8).makespan + 1e-9
+    assert t_bal <= S.place(S.min_gpu_queue(configs, 8, tm, mem), 8).makespan + 1e-9
