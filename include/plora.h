@@ -188,6 +188,17 @@ PLORA_API int plora_rope(void* stream, const void* in, void* out, const float* c
 PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* logits,
                                   const int64_t* labels, const float* weight, float* tok_loss);
 
+/* Vocabulary-parallel cross entropy (tensor-parallel lm_head, config C4): logits
+ * [rows][V] hold vocabulary slice [v0, v0+V) of each row.
+ *   plora_ce_stats : stats[rows][3] = (max_v x, sum_v exp(x - max), x[label] if
+ *                    label in the slice else 0); the caller all-reduces these across
+ *                    the tensor-parallel group to get lse = M + log(S').
+ *   plora_ce_apply : overwrites the slice with weight_t * (exp(x - lse_t) - onehot). */
+PLORA_API int plora_ce_stats(void* stream, int64_t rows, int64_t V, const void* logits,
+                             const int64_t* labels, int64_t v0, float* stats);
+PLORA_API int plora_ce_apply(void* stream, int64_t rows, int64_t V, void* logits,
+                             const int64_t* labels, int64_t v0, const float* lse, const float* weight);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,8 @@ EXPORTS = (
     "plora_swiglu_bwd",
     "plora_rope",
     "plora_cross_entropy",
+    "plora_ce_stats",
+    "plora_ce_apply",
 )
 
 ABI_VERSION = 2
@@ -100,6 +102,8 @@ _SIGNATURES = {
     "plora_rope": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _i32],
                    ctypes.c_int),
     "plora_cross_entropy": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "plora_ce_stats": ([_vp, _i64, _i64, _vp, _vp, _i64, _vp], ctypes.c_int),
+    "plora_ce_apply": ([_vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp], ctypes.c_int),
 }
 
 

@@ -55,11 +55,16 @@ class AdapterBank:
                  weight_decay: float | Sequence[float] = 0.0, device="cuda",
                  betas=(0.9, 0.999), eps: float = 1e-8, seeds: Sequence[int] | None = None,
                  init: str = "bench", a_scale: float | None = None, b_std: float | Sequence[float] = 0.02,
-                 chunk_elems: int = 8192):
+                 chunk_elems: int = 8192, full_targets: Sequence[Target] | None = None, shard=None):
         self.meta = meta
         self.n = meta.n_adapters
         self.n_layers = n_layers
         self.targets = list(targets)
+        # tensor parallel (tp.py): ``targets`` are this rank's local shapes; the initial
+        # values are drawn at the full shapes (same RNG stream as an unsharded bank) and
+        # sliced, so TP shards are exact slices of the unsharded adapters.
+        self.full_targets = list(full_targets) if full_targets is not None else self.targets
+        self.shard = shard
         self.device = torch.device(device)
         self.betas = betas
         self.eps = eps
@@ -146,11 +151,14 @@ class AdapterBank:
         for i, seed in enumerate(seeds):
             g = torch.Generator(device=self.device).manual_seed(int(seed))
             for layer in range(self.n_layers):
-                for t in self.targets:
+                for t, ft in zip(self.targets, self.full_targets):
                     r = m.ranks[i]
-                    bound = a_scale if a_scale is not None else 1.0 / math.sqrt(t.h_in)
-                    a = (torch.rand(t.h_in, r, generator=g, device=self.device) * 2 - 1) * bound
-                    b = torch.randn(t.h_out, r, generator=g, device=self.device) * b_stds[i]
+                    bound = a_scale if a_scale is not None else 1.0 / math.sqrt(ft.h_in)
+                    a = (torch.rand(ft.h_in, r, generator=g, device=self.device) * 2 - 1) * bound
+                    b = torch.randn(ft.h_out, r, generator=g, device=self.device) * b_stds[i]
+                    if self.shard is not None:
+                        a = a[self.shard.lora_rows(t.name, "A", ft.h_in, ft.h_out)]
+                        b = b[self.shard.lora_rows(t.name, "B", ft.h_in, ft.h_out)]
                     self.block(self.P, layer, t.name, "A", i)[:, :r] = a
                     self.block(self.P, layer, t.name, "B", i)[:, :r] = b
         self.refresh_shadow()

@@ -329,6 +329,82 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(bf16* __restrict__ logit
   }
 }
 
+
+// ---------------------------------------------------------------- vocab-parallel cross entropy
+// Tensor-parallel lm_head (config C4): each rank holds logits for vocabulary slice
+// [v0, v0+V).  Pass 1 writes per-row (max, sum exp(x - max), x[label] if the label is
+// in this slice else 0); the host all-reduces them across the TP group (max, then the
+// rescaled sums and label logits); pass 2 overwrites the slice with
+// w_t (softmax - onehot(label)) given the global lse.
+__global__ void __launch_bounds__(kCeThreads) ce_stats_kernel(const bf16* __restrict__ logits,
+                                                              const int64_t* __restrict__ labels,
+                                                              float* __restrict__ stats, int V, int64_t v0) {
+  __shared__ float red[kCeThreads / 32];
+  __shared__ float redm[kCeThreads / 32];
+  const int64_t row = blockIdx.x;
+  const bf16* x = logits + row * (int64_t)V;
+  const int nv = V / 8;
+  float m = -INFINITY, sum = 0.f;
+  for (int i = threadIdx.x; i < nv; i += kCeThreads) {
+    float f[8];
+    load8(x + i * 8, f);
+    float lm = f[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) lm = fmaxf(lm, f[e]);
+    if (lm > m) {
+      sum *= __expf(m - lm);
+      m = lm;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sum += __expf(f[e] - m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o);
+    const float os = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float nm = fmaxf(m, om);
+    sum = (m == -INFINITY ? 0.f : sum * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int wid = threadIdx.x / 32, lid = threadIdx.x % 32;
+  if (lid == 0) {
+    redm[wid] = m;
+    red[wid] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kCeThreads / 32; ++i) M = fmaxf(M, redm[i]);
+    float S = 0.f;
+#pragma unroll
+    for (int i = 0; i < kCeThreads / 32; ++i) S += (redm[i] == -INFINITY) ? 0.f : red[i] * __expf(redm[i] - M);
+    const int64_t lab = labels[row] - v0;
+    stats[row * 3 + 0] = M;
+    stats[row * 3 + 1] = S;
+    stats[row * 3 + 2] = (lab >= 0 && lab < V) ? __bfloat162float(x[lab]) : 0.f;
+  }
+}
+
+__global__ void ce_apply_kernel(bf16* __restrict__ logits, const int64_t* __restrict__ labels,
+                                const float* __restrict__ lse, const float* __restrict__ weight, int V,
+                                int64_t v0) {
+  const int64_t row = blockIdx.x;
+  bf16* x = logits + row * (int64_t)V;
+  const float w = weight[row];
+  const float l = lse[row];
+  const int64_t lab = labels[row] - v0;
+  for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
+    float f[8];
+    load8(x + i * 8, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = w * __expf(f[e] - l);
+    const int64_t base = (int64_t)i * 8;
+    if (lab >= base && lab < base + 8) f[lab - base] -= w;
+    store8(x + i * 8, f);
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -413,6 +489,24 @@ PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* l
   ce_kernel<<<rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<bf16*>(logits), labels, weight, tok_loss, (int)V);
   return launch_status("cross_entropy");
+}
+
+PLORA_API int plora_ce_stats(void* stream, int64_t rows, int64_t V, const void* logits, const int64_t* labels,
+                             int64_t v0, float* stats) {
+  if (rows <= 0) return 0;
+  if (V % 8) return plora::set_error("ce_stats: V must be a multiple of 8");
+  ce_stats_kernel<<<rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(logits), labels, stats, (int)V, v0);
+  return launch_status("ce_stats");
+}
+
+PLORA_API int plora_ce_apply(void* stream, int64_t rows, int64_t V, void* logits, const int64_t* labels,
+                             int64_t v0, const float* lse, const float* weight) {
+  if (rows <= 0) return 0;
+  if (V % 8) return plora::set_error("ce_apply: V must be a multiple of 8");
+  ce_apply_kernel<<<rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<bf16*>(logits), labels, lse,
+                                                                     weight, (int)V, v0);
+  return launch_status("ce_apply");
 }
 
 }  // extern "C"

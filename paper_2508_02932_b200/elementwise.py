@@ -105,6 +105,29 @@ def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, weight: torch.Tens
     _LAUNCHES[0] += 1
 
 
+def ce_stats(logits: torch.Tensor, labels: torch.Tensor, v0: int, stats: torch.Tensor | None = None):
+    """Vocabulary-parallel CE pass 1: stats [rows][3] f32 = (max, sum exp(x - max), x[label] or 0)
+    over this rank's vocabulary slice [v0, v0 + V)."""
+    rows, V = logits.shape
+    if stats is None:
+        stats = torch.empty((rows, 3), dtype=torch.float32, device=logits.device)
+    _lib.check(_lib.lib().plora_ce_stats(_stream(), rows, V, _need(logits, "logits"),
+                                         _need(labels, "labels", torch.int64), int(v0),
+                                         _need(stats, "stats", torch.float32)), "ce_stats")
+    _LAUNCHES[0] += 1
+    return stats
+
+
+def ce_apply(logits: torch.Tensor, labels: torch.Tensor, v0: int, lse: torch.Tensor, weight: torch.Tensor):
+    """Vocabulary-parallel CE pass 2: logits <- weight_t (exp(x - lse_t) - onehot_t) on the slice."""
+    rows, V = logits.shape
+    _lib.check(_lib.lib().plora_ce_apply(_stream(), rows, V, _need(logits, "logits"),
+                                         _need(labels, "labels", torch.int64), int(v0),
+                                         _need(lse, "lse", torch.float32), _need(weight, "weight", torch.float32)),
+               "ce_apply")
+    _LAUNCHES[0] += 1
+
+
 # ---------------------------------------------------------------------------- torch references
 def ref_rmsnorm_fwd(x, w, eps):
     xf = x.float()

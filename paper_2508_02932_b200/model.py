@@ -33,6 +33,7 @@ from . import elementwise as ew
 from . import ops
 from .adapters import AdapterBank, Target
 from .meta import PackMeta, build_meta
+from .tp import Comm, TPShard
 
 bf16 = torch.bfloat16
 
@@ -82,6 +83,9 @@ PRESETS = {
     # C1: tiny 2-layer transformer, runs on the CPU reference
     "tiny": ModelConfig("tiny-d256", d=256, n_layers=2, ffn=1024, n_heads=4, n_kv=4, vocab=1024,
                         rope_theta=10000.0),
+    # C1 variant with the Qwen2 features C2/C4 use: GQA, q/k/v bias, tied embeddings
+    "tiny-qwen": ModelConfig("tiny-qwen-d256", d=256, n_layers=2, ffn=768, n_heads=4, n_kv=2, vocab=1024,
+                             tied=True, rope_theta=1000000.0, norm_eps=1e-6, qkv_bias=True),
     # C2: Qwen2.5-3B (tied embeddings, q/k/v bias)
     "qwen2.5-3b": ModelConfig("Qwen2.5-3B", d=2048, n_layers=36, ffn=11008, n_heads=16, n_kv=2,
                               vocab=151936, tied=True, rope_theta=1000000.0, norm_eps=1e-6, qkv_bias=True),
@@ -108,7 +112,7 @@ class AdapterSpec:
 def bench_adapters(cfg_name: str) -> tuple[list[AdapterSpec], int]:
     mults = [0.25, 1.0, 2.0, 4.0]
     lrs = [2e-5, 5e-5, 1e-4, 2e-4, 4e-4]
-    if cfg_name == "tiny":
+    if cfg_name in ("tiny", "tiny-qwen"):
         ranks, batch, s = [8, 16, 32, 64], [1, 2, 1, 2], 128
     elif cfg_name == "qwen2.5-3b":
         ranks, batch, s = [8, 16, 32, 64] * 2, [1, 2, 4, 1, 2, 4, 1, 2], 1024
@@ -128,29 +132,41 @@ class BaseWeights:
     """Frozen bf16 base model (random init N(0, 0.02^2), seed 0; norms = 1).
     Projection weights use the nn.Linear layout [h_out][h_in] (K-major operand)."""
 
-    def __init__(self, cfg: ModelConfig, device="cuda", seed: int = 0, std: float = 0.02):
+    def __init__(self, cfg: ModelConfig, device="cuda", seed: int = 0, std: float = 0.02,
+                 shard: TPShard | None = None):
+        """``shard``: keep only this tensor-parallel rank's slices (tp.py).  Every tensor
+        is drawn at its full shape from the same RNG stream and then sliced, so the
+        shards of a TP group are exact slices of the unsharded model."""
         self.cfg = cfg
+        self.shard = shard or TPShard()
+        sh = self.shard
         g = torch.Generator(device=device).manual_seed(seed)
 
         def rnd(*shape):
             return (torch.randn(*shape, generator=g, device=device) * std).to(bf16)
 
-        self.embed = rnd(cfg.vocab, cfg.d)
+        self.embed = rnd(cfg.vocab, cfg.d)    # replicated (token gather)
         self.layers = []
         for _ in range(cfg.n_layers):
-            lw = {t.name: rnd(t.h_out, t.h_in) for t in cfg.targets()}
+            lw = {}
+            for t in cfg.targets():
+                rows, cols = sh.weight_slice(t.name, t.h_in, t.h_out)
+                lw[t.name] = rnd(t.h_out, t.h_in)[rows, cols].contiguous()
             lw["attn_norm"] = torch.ones(cfg.d, device=device, dtype=bf16)
             lw["mlp_norm"] = torch.ones(cfg.d, device=device, dtype=bf16)
             if cfg.qkv_bias:
-                for t in ("q", "k", "v"):
-                    lw[t + "_bias"] = rnd(lw[t].shape[0])
+                for t in cfg.targets()[:3]:
+                    lw[t.name + "_bias"] = rnd(t.h_out)[sh.span(t.h_out)].contiguous()
             self.layers.append(lw)
         self.final_norm = torch.ones(cfg.d, device=device, dtype=bf16)
-        self.lm_head = self.embed if cfg.tied else rnd(cfg.vocab, cfg.d)
+        vs = sh.span(cfg.vocab)
+        # vocabulary-parallel lm_head: rows [v0, v0 + V/tp) of [V][d]
+        self.lm_head = self.embed[vs] if cfg.tied else rnd(cfg.vocab, cfg.d)[vs].contiguous()
+        self.vocab_start = vs.start
 
     def nbytes(self) -> int:
         n = self.embed.numel() + self.final_norm.numel()
-        if not self.cfg.tied:
+        if self.lm_head.data_ptr() != self.embed.data_ptr():
             n += self.lm_head.numel()
         for lw in self.layers:
             n += sum(v.numel() for v in lw.values())
@@ -191,8 +207,19 @@ class PackedLoraTrainer:
 
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
-                 a_scale: float | None = None, b_std: float | Sequence[float] = 0.02):
+                 a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None):
+        """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
+        tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
+        the step inserts the all-reduces described in tp.py."""
         self.cfg = cfg
+        self.tp = tp if (tp is not None and tp.world > 1) else None
+        self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
+        g = self.shard.world
+        if cfg.n_heads % g or cfg.n_kv % g:
+            raise ValueError(f"tp={g} must divide n_heads={cfg.n_heads} and n_kv={cfg.n_kv}")
+        self.H_l, self.KV_l = cfg.n_heads // g, cfg.n_kv // g
+        self.targets = [Target(t.name, t.h_in, t.h_out // g) if self.shard.kind(t.name) == "col"
+                        else Target(t.name, t.h_in // g, t.h_out) for t in cfg.targets()]
         self.specs = list(specs)
         self.s = seq_len
         self.device = torch.device(device)
@@ -200,10 +227,13 @@ class PackedLoraTrainer:
         self.meta: PackMeta = build_meta([sp.rank for sp in specs], tokens, [sp.alpha for sp in specs]).to(
             self.device)
         self.T = self.meta.total_tokens
-        self.base = base or BaseWeights(cfg, self.device)
-        self.bank = AdapterBank(self.meta, cfg.n_layers, cfg.targets(), [sp.lr for sp in specs],
+        self.base = base or BaseWeights(cfg, self.device, shard=self.shard)
+        if self.base.shard != self.shard:
+            raise ValueError("base weights are sharded for a different tensor-parallel position")
+        self.bank = AdapterBank(self.meta, cfg.n_layers, self.targets, [sp.lr for sp in specs],
                                 [sp.weight_decay for sp in specs], device=self.device, seeds=adapter_seeds,
-                                a_scale=a_scale, b_std=b_std)
+                                a_scale=a_scale, b_std=b_std, full_targets=cfg.targets(),
+                                shard=self.shard if self.tp is not None else None)
         self.cos, self.sin = rope_tables(cfg, seq_len, self.device)
         self.ce_chunk = ce_chunk
         # per-token adapter id and the CE weight 1/n_i (labels exist for s-1 tokens per sequence)
@@ -232,6 +262,29 @@ class PackedLoraTrainer:
                               bank.region_flat(bank.G, layer, tname, "B"),
                               dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
 
+    def _lin_bwd_col(self, layer: int, tname: str, x, w, hs, dy, dx_residual=None, dx_out=None, need_dx=True):
+        """Column-parallel backward under TP: dH_s is partial, so dA needs the
+        all-reduced dH (tp.py); dB_s and the partial dX_s are local."""
+        if self.tp is None:
+            return self._lin_bwd(layer, tname, x, w, hs, dy, need_dx=need_dx, dx_residual=dx_residual,
+                                 dx_out=dx_out)
+        bank, meta = self.bank, self.meta
+        dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
+        ops.shrink(meta, dy, bank.shadow_of(layer, tname, "B"), dh)                       # partial dH_s
+        ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, tname, "B"))             # dB_s (local)
+        dx = None
+        if need_dx:
+            dx = ops.linear_expand(meta, dy, w, False, bank.shadow_of(layer, tname, "A"), dh,  # partial dX_s
+                                   dx_out, dx_residual)
+        self.tp.all_reduce_(dh)
+        ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A"))              # dA (replicated)
+        return dx
+
+    def _reduce(self, *ts):
+        if self.tp is not None:
+            for t in ts:
+                self.tp.all_reduce_(t)
+
     # ------------------------------------------------------------------ forward
     def _layer_fwd(self, layer: int, h_prev: torch.Tensor, delta: torch.Tensor | None
                    ) -> tuple[torch.Tensor, torch.Tensor, _LayerSave]:
@@ -239,7 +292,7 @@ class PackedLoraTrainer:
         the fused add+RMSNorm); returns (h_mid, down_out) -- this layer's output is their
         sum, materialised by the next layer's (or the final) add+RMSNorm."""
         cfg, lw = self.cfg, self.base.layers[layer]
-        T, hd, H, KV, s = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv, self.s
+        T, hd, H, KV, s = self.T, cfg.head_dim, self.H_l, self.KV_l, self.s
         B = T // s
         if delta is None:
             h = h_prev
@@ -263,6 +316,7 @@ class PackedLoraTrainer:
             og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
         attn = ew.rope(og.detach().transpose(1, 2), self.cos, self.sin, s, rotate=False)   # [T][H*hd]
         o_out, hs_o = self._lin_fwd(layer, "o", attn, lw["o"])
+        self._reduce(o_out, hs_o)                      # row-parallel (TP): Y and Hs are partial sums
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
         g, hs_g = self._lin_fwd(layer, "gate", x2, lw["gate"])
@@ -270,6 +324,7 @@ class PackedLoraTrainer:
         del x2
         act = ew.swiglu_fwd(g, u)
         d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
+        self._reduce(d_out, hs_d)
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
                           attn_out=attn, g=g, u=u,
                           hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d})
@@ -278,7 +333,7 @@ class PackedLoraTrainer:
     # ------------------------------------------------------------------ backward
     def _layer_bwd(self, layer: int, sv: _LayerSave, dh: torch.Tensor, need_dx: bool) -> torch.Tensor:
         cfg, lw = self.cfg, self.base.layers[layer]
-        T, hd, H, KV, s = self.T, cfg.head_dim, cfg.n_heads, cfg.n_kv, self.s
+        T, hd, H, KV, s = self.T, cfg.head_dim, self.H_l, self.KV_l, self.s
         B = T // s
         # MLP: h_out = h_mid + down(swiglu(gate(x2), up(x2)))
         act = ew.swiglu_fwd(sv.g, sv.u)                                   # recompute
@@ -287,8 +342,9 @@ class PackedLoraTrainer:
         del d_act
         x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
         del act
-        dx2 = self._lin_bwd(layer, "up", x2, lw["up"], sv.hs["up"], du)
-        dx2 = self._lin_bwd(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
+        dx2 = self._lin_bwd_col(layer, "up", x2, lw["up"], sv.hs["up"], du)
+        dx2 = self._lin_bwd_col(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
+        self._reduce(dx2)
         del dg, du, x2
         d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh, out=dx2)
         # attention: h_mid = h_in + o(attn(rope(q(x1)), rope(k(x1)), v(x1)))
@@ -300,12 +356,15 @@ class PackedLoraTrainer:
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
         dv = ew.rope(dv.transpose(1, 2), self.cos, self.sin, s, rotate=False)
         x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
-        dx1 = self._lin_bwd(layer, "v", x1, lw["v"], sv.hs["v"], dv)
-        dx1 = self._lin_bwd(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1)
-        dx1 = self._lin_bwd(layer, "q", x1, lw["q"], sv.hs["q"], dq, dx_residual=dx1, dx_out=dx1)
+        dx1 = self._lin_bwd_col(layer, "v", x1, lw["v"], sv.hs["v"], dv, need_dx=need_dx)
+        dx1 = self._lin_bwd_col(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1,
+                                need_dx=need_dx)
+        dx1 = self._lin_bwd_col(layer, "q", x1, lw["q"], sv.hs["q"], dq, dx_residual=dx1, dx_out=dx1,
+                                need_dx=need_dx)
         del dq, dk, dv, x1
-        if not need_dx:
+        if not need_dx:   # first layer: the embedding is frozen, no input gradient
             return None
+        self._reduce(dx1)
         return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid, out=dx1)
 
     # ------------------------------------------------------------------ loss head
@@ -320,9 +379,22 @@ class PackedLoraTrainer:
         for c0 in range(0, self.T, self.ce_chunk):
             c1 = min(self.T, c0 + self.ce_chunk)
             logits = ops.gemm(xf[c0:c1], self.base.lm_head, True)
-            ew.cross_entropy(logits, labels[c0:c1], self.ce_weight[c0:c1], tok_loss[c0:c1])
+            if self.tp is None:
+                ew.cross_entropy(logits, labels[c0:c1], self.ce_weight[c0:c1], tok_loss[c0:c1])
+            else:   # vocabulary-parallel CE: per-row (max, sumexp, label logit) across the TP group
+                v0 = self.base.vocab_start
+                st = ew.ce_stats(logits, labels[c0:c1], v0)
+                m = st[:, 0].contiguous()
+                self.tp.all_reduce_(m, "max")
+                sl = torch.stack((st[:, 1] * torch.exp(st[:, 0] - m), st[:, 2]), 1)
+                self.tp.all_reduce_(sl)
+                lse = m + torch.log(sl[:, 0])
+                w = self.ce_weight[c0:c1]
+                ew.ce_apply(logits, labels[c0:c1], v0, lse, w)
+                tok_loss[c0:c1] = w * (lse - sl[:, 1])
             ops.gemm(logits, self.base.lm_head, False, out=dxf[c0:c1])   # dX = dlogits @ W_lm
             del logits
+        self._reduce(dxf)
         # per-adapter sums over contiguous segments (deterministic prefix-sum differences)
         cs = torch.cumsum(tok_loss.double(), 0)
         cs = torch.cat((cs.new_zeros(1), cs))

@@ -1,0 +1,171 @@
+"""Tensor-parallel packed LoRA (config C4: a base too large for one job's GPU is
+Megatron-sharded over NVLink).
+
+The reference only models TP as a memory divisor (``ShardingSpec.d_tp``,
+workload.py:106-128; ``costmodel.py:120-124``) and the paper runs it through
+PyTorch DTensor.  Here the packed trainer itself shards:
+
+  column-parallel (q, k, v, gate, up): W split along h_out; LoRA A replicated,
+      B split along h_out.  Forward: no collective (Hs = alpha X A is computed
+      identically on every rank).  Backward: dH_s = alpha dY_s B_s^T is partial,
+      so dH is all-reduced (T x 64nb bf16, small) before dA = X^T dH; the input
+      gradient dX_s = dY_s W_s + dH_s A^T is partial and all-reduced once per
+      shared input (q+k+v, gate+up).
+  row-parallel (o, down): W split along h_in; LoRA A split along h_in, B
+      replicated.  Forward: Y_s = X_s W_s^T + Hs_s B^T with the partial Hs_s, so
+      one all-reduce of Y gives X W^T + (sum_s Hs_s) B^T by linearity; Hs itself
+      is all-reduced (small) for dB = Hs^T dY.  Backward: no collective.
+  lm_head: vocabulary-parallel with a two-pass cross entropy
+      (``plora_ce_stats`` / ``plora_ce_apply``).
+
+Replicated LoRA factors (column A, row B) get bit-identical gradients on every
+rank (identical inputs + deterministic kernels + all-reduced dH / Hs), so their
+AdamW states evolve identically without a gradient all-reduce.
+
+Communicators: ``DistComm`` wraps a torch.distributed process group (NCCL over
+NVLink/NVSwitch on the box; gloo in CPU tests).  ``ThreadComm`` runs a TP group
+of g ranks as g threads sharing ONE GPU (each on its own stream) with a
+deterministic fixed-order sum -- it is how the sharded path is parity-tested on
+a single B200 (gpurun gives one GPU).
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+
+COLUMN = ("q", "k", "v", "gate", "up")
+ROW = ("o", "down")
+
+
+@dataclass(frozen=True)
+class TPShard:
+    """Position of one rank in a tensor-parallel group of ``world`` ranks."""
+    rank: int = 0
+    world: int = 1
+
+    def span(self, n: int) -> slice:
+        if n % self.world:
+            raise ValueError(f"dimension {n} is not divisible by tp={self.world}")
+        per = n // self.world
+        return slice(self.rank * per, (self.rank + 1) * per)
+
+    def kind(self, target: str) -> str:
+        return "col" if target in COLUMN else "row"
+
+    def weight_slice(self, target: str, h_in: int, h_out: int) -> tuple[slice, slice]:
+        """(rows, cols) of the nn.Linear-layout weight [h_out][h_in] this rank owns."""
+        if self.kind(target) == "col":
+            return self.span(h_out), slice(0, h_in)
+        return slice(0, h_out), self.span(h_in)
+
+    def lora_rows(self, target: str, kind: str, h_in: int, h_out: int) -> slice:
+        """Rows of the LoRA factor this rank owns: A is [h_in][r], B^T is [h_out][r]."""
+        if kind == "A":
+            return self.span(h_in) if self.kind(target) == "row" else slice(0, h_in)
+        return self.span(h_out) if self.kind(target) == "col" else slice(0, h_out)
+
+    def replicated(self, target: str, kind: str) -> bool:
+        return (kind == "A") == (self.kind(target) == "col")
+
+
+class Comm:
+    """Minimal collective interface the TP trainer needs (in-place all-reduce)."""
+    rank: int = 0
+    world: int = 1
+
+    def all_reduce_(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+
+class DistComm(Comm):
+    """torch.distributed process group (backend nccl on GPU, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self._dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_reduce_(self, t, op="sum"):
+        d = self._dist
+        d.all_reduce(t, op=d.ReduceOp.SUM if op == "sum" else d.ReduceOp.MAX, group=self.group)
+        return t
+
+
+class _ThreadGroup:
+    def __init__(self, world: int):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots: list = [None] * world
+        self.result = None
+
+
+class ThreadComm(Comm):
+    """One rank of a TP group emulated by threads on a single GPU (tests / smoke).
+
+    all_reduce_: every rank synchronises its stream, deposits its tensor, rank 0 sums
+    in fixed rank order in fp32 (deterministic) and every rank copies the result."""
+
+    def __init__(self, group: _ThreadGroup, rank: int):
+        self.g = group
+        self.rank = rank
+        self.world = group.world
+
+    def all_reduce_(self, t, op="sum"):
+        g = self.g
+        if t.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        g.slots[self.rank] = t
+        g.barrier.wait()
+        if self.rank == 0:
+            acc = g.slots[0].float().clone()
+            for other in g.slots[1:]:
+                o = other.float()
+                acc = acc + o if op == "sum" else torch.maximum(acc, o)
+            g.result = acc
+            if t.is_cuda:
+                torch.cuda.current_stream().synchronize()
+        g.barrier.wait()
+        t.copy_(g.result)
+        if t.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        g.barrier.wait()   # everyone has read the result before any rank deposits again
+        return t
+
+
+def run_threaded(world: int, fn: Callable[[Comm], object]) -> list:
+    """Run fn(comm) for every rank of a ThreadComm group; returns per-rank results.
+    Each rank gets its own CUDA stream (if CUDA is available)."""
+    group = _ThreadGroup(world)
+    results: list = [None] * world
+    errors: list = []
+
+    def body(r):
+        comm = ThreadComm(group, r)
+        try:
+            if torch.cuda.is_available():
+                torch.cuda.set_device(0)
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    results[r] = fn(comm)
+                    torch.cuda.current_stream().synchronize()
+            else:
+                results[r] = fn(comm)
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            errors.append(exc)
+            group.barrier.abort()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        real = [e for e in errors if not isinstance(e, threading.BrokenBarrierError)]
+        raise (real or errors)[0]
+    return results

@@ -18,14 +18,14 @@ from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapte
 pytestmark = pytest.mark.gpu
 
 
-def _trainer(specs=None, seeds=None):
+def _trainer(specs=None, seeds=None, preset="tiny"):
     """C1 with the bench ranks/alphas (alpha = r * {0.25,1,2,4} up to 256).  B_i is drawn
     with std 0.2/alpha_i so every adapter's low-rank term is O(1) next to the base path:
     with B ~ N(0, 0.05^2) the alpha=256 adapter's term is ~100x the base output, the
     random-weight network saturates its attention and the bf16-vs-fp64 comparison
     measures chaos, not the kernels."""
-    cfg = PRESETS["tiny"]
-    sp, s = bench_adapters("tiny")
+    cfg = PRESETS[preset]
+    sp, s = bench_adapters(preset)
     specs = specs or sp
     return PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=seeds, a_scale=0.05,
                              b_std=[0.2 / x.alpha for x in specs])
@@ -39,8 +39,11 @@ def _oracle(tr, tokens):
                        tokens.cpu(), tr.s, cos, sin, n_lab)
 
 
-def test_tiny_model_matches_oracle():
-    tr = _trainer()
+@pytest.mark.parametrize("preset", ["tiny", "tiny-qwen"])
+def test_tiny_model_matches_oracle(preset):
+    """tiny = C1 (Llama-style); tiny-qwen = the same size with C2/C4's Qwen2 features
+    (GQA 4/2, q/k/v bias, tied embeddings)."""
+    tr = _trainer(preset=preset)
     tokens = tr.synthetic_tokens().cuda()
     losses = tr.forward_backward(tokens).cpu().double()
     ref_losses, ref_grads, _ = _oracle(tr, tokens)

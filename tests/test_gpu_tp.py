@@ -1,0 +1,115 @@
+"""Tensor-parallel packed LoRA (config C4's path) on ONE B200: a TP group of g ranks
+runs as g threads sharing the GPU (tp.ThreadComm, each rank on its own stream, the
+same sharded kernels and all-reduce placement the NCCL path uses).  The sharded
+job must reproduce the unsharded packed trainer (itself parity-pinned to the fp64
+oracle in test_gpu_model.py):
+
+  per-adapter loss                     |d| / |ref| <= 1e-2
+  per-(layer, target, factor, adapter) gradient, shards reassembled:
+                                       relative Frobenius <= 3e-2 (pooled <= 2e-2)
+  replicated factors (column A, row B) bit-identical on every rank, before and
+  after a fused AdamW step (no gradient all-reduce is needed for them)."""
+
+import pytest
+import torch
+
+from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
+from paper_2508_02932_b200.tp import TPShard, run_threaded
+
+pytestmark = pytest.mark.gpu
+
+
+def _make(preset, tp=None):
+    cfg = PRESETS[preset]
+    specs, s = bench_adapters(preset)
+    return PackedLoraTrainer(cfg, specs, s, device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in specs],
+                             tp=tp)
+
+
+def _grads(tr):
+    out = {}
+    bank = tr.bank
+    for layer in range(tr.cfg.n_layers):
+        for t in bank.targets:
+            for kind in ("A", "B"):
+                for i in range(tr.meta.n_adapters):
+                    r = tr.meta.ranks[i]
+                    out[(layer, t.name, kind, i)] = bank.block(bank.G, layer, t.name, kind, i)[:, :r].float().cpu()
+    return out
+
+
+def _masters(tr):
+    bank = tr.bank
+    return {(layer, t.name, kind, i): bank.block(bank.P, layer, t.name, kind, i).cpu().clone()
+            for layer in range(tr.cfg.n_layers) for t in bank.targets for kind in ("A", "B")
+            for i in range(tr.meta.n_adapters)}
+
+
+@pytest.mark.parametrize("preset,g", [("tiny-qwen", 2), ("tiny", 4)])
+def test_tp_matches_unsharded(preset, g):
+    ref = _make(preset)
+    tokens = ref.synthetic_tokens().cuda()
+    ref_losses = ref.forward_backward(tokens).double().cpu()
+    ref_grads = _grads(ref)
+
+    def rank_fn(comm):
+        tr = _make(preset, tp=comm)
+        losses = tr.forward_backward(tokens).double().cpu()
+        grads = _grads(tr)
+        tr.bank.adamw_step()
+        torch.cuda.current_stream().synchronize()
+        return losses, grads, _masters(tr)
+
+    outs = run_threaded(g, rank_fn)
+    for losses, _, _ in outs:
+        rel = ((losses - ref_losses).abs() / ref_losses.abs()).max().item()
+        assert rel <= 1e-2, (rel, losses, ref_losses)
+    # every rank computes identical losses (all-reduced CE statistics)
+    for losses, _, _ in outs[1:]:
+        assert torch.equal(losses, outs[0][0])
+
+    num = den = worst = 0.0
+    for key, want in ref_grads.items():
+        layer, tname, kind, i = key
+        sh = TPShard(0, g)
+        if sh.replicated(tname, kind):
+            got = outs[0][1][key]
+            for r in range(1, g):
+                assert torch.equal(outs[r][1][key], got), key      # bit-identical replicas
+                assert torch.equal(outs[r][2][key], outs[0][2][key]), key
+        else:
+            got = torch.cat([outs[r][1][key] for r in range(g)], 0)
+        assert got.shape == want.shape, (key, got.shape, want.shape)
+        e = (got - want).norm().item()
+        rn = want.norm().item()
+        num += e * e
+        den += rn * rn
+        worst = max(worst, e / max(rn, 1e-30))
+    print(f"tp={g} {preset}: worst per-block grad rel-Frob {worst:.3e}, pooled {(num / den) ** 0.5:.3e}")
+    assert worst <= 3e-2
+    assert (num / den) ** 0.5 <= 2e-2
+
+
+def test_tp_shards_are_slices_of_unsharded_model():
+    """Sharded base weights / adapter masters are exact slices of the unsharded ones."""
+    ref = _make("tiny-qwen")
+
+    def rank_fn(comm):
+        tr = _make("tiny-qwen", tp=comm)
+        torch.cuda.current_stream().synchronize()
+        return tr
+
+    trs = run_threaded(2, rank_fn)
+    cfg = ref.cfg
+    for r, tr in enumerate(trs):
+        sh = TPShard(r, 2)
+        for layer in range(cfg.n_layers):
+            for t in cfg.targets():
+                rows, cols = sh.weight_slice(t.name, t.h_in, t.h_out)
+                assert torch.equal(tr.base.layers[layer][t.name], ref.base.layers[layer][t.name][rows, cols])
+                for kind in ("A", "B"):
+                    for i in range(ref.meta.n_adapters):
+                        sl = sh.lora_rows(t.name, kind, t.h_in, t.h_out)
+                        assert torch.equal(tr.bank.block(tr.bank.P, layer, t.name, kind, i),
+                                           ref.bank.block(ref.bank.P, layer, t.name, kind, i)[sl])
+        assert torch.equal(tr.base.lm_head, ref.base.lm_head[sh.span(cfg.vocab)])
