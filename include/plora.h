@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 2
+#define PLORA_ABI_VERSION 3
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -173,10 +173,12 @@ PLORA_API int plora_add_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const
 /* dx = rstd * (g - xhat * mean(g * xhat)) (+ residual), g = dy * w. */
 PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const void* dy, const void* x,
                                 const float* rstd, const void* w, const void* residual, void* dx);
-/* a = silu(g) * u ;  (dg, du) from da. n elements, multiple of 8. */
+/* a = silu(g) * u ;  (dg, du) from da. n elements, multiple of 8.  The backward may
+ * also re-emit a (act may be NULL) in the same pass, so the down-projection's
+ * dA = a^T dH needs no separate recompute of the activation; dg / du may alias g / u. */
 PLORA_API int plora_swiglu_fwd(void* stream, int64_t n, const void* g, const void* u, void* a);
 PLORA_API int plora_swiglu_bwd(void* stream, int64_t n, const void* da, const void* g, const void* u,
-                               void* dg, void* du);
+                               void* dg, void* du, void* act);
 /* out[t][h][:] = rope(in[b][h][p][:]) (t = b*s + p; element strides sb, sp, sh), half
  * rotation with cos/sin [s][hd/2] f32; inverse = 1 rotates by -theta (backward);
  * rotate = 0 performs only the layout change.  out is contiguous [T][H][hd]. */

@@ -9,10 +9,12 @@ math).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libplora.so"
+LIB_PATH = Path(os.environ.get("PLORA_LIB", "")).resolve() if os.environ.get("PLORA_LIB") else \
+    Path(__file__).resolve().parent / "libplora.so"   # PLORA_LIB: A/B experiments with another build
 
 # Every symbol include/plora.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -39,7 +41,7 @@ EXPORTS = (
     "plora_ce_apply",
 )
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class PloraError(RuntimeError):
@@ -98,7 +100,7 @@ _SIGNATURES = {
     "plora_add_rmsnorm_fwd": ([_vp, _i64, _i64, _vp, _vp, _vp, _f32, _vp, _vp, _vp], ctypes.c_int),
     "plora_rmsnorm_bwd": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "plora_swiglu_fwd": ([_vp, _i64, _vp, _vp, _vp], ctypes.c_int),
-    "plora_swiglu_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "plora_swiglu_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "plora_rope": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _i32],
                    ctypes.c_int),
     "plora_cross_entropy": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp], ctypes.c_int),

@@ -192,9 +192,9 @@ __global__ void swiglu_fwd_kernel(const bf16* __restrict__ g, const bf16* __rest
   }
 }
 
-__global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* __restrict__ g,
-                                  const bf16* __restrict__ u, bf16* __restrict__ dg,
-                                  bf16* __restrict__ du, int64_t n8) {
+__global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* g, const bf16* u, bf16* dg,
+                                  bf16* du, bf16* __restrict__ act,
+                                  int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     float af[8], gf[8], uf[8], og[8], ou[8];
     load8(da + i * 8, af);
@@ -205,6 +205,12 @@ __global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* __res
       const float s = 1.f / (1.f + __expf(-gf[e]));
       ou[e] = af[e] * gf[e] * s;
       og[e] = af[e] * uf[e] * s * (1.f + gf[e] * (1.f - s));
+    }
+    if (act) {   // same arithmetic as swiglu_fwd_kernel: bit-identical activation
+      float a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = gf[e] / (1.f + __expf(-gf[e])) * uf[e];
+      store8(act + i * 8, a);
     }
     store8(dg + i * 8, og);
     store8(du + i * 8, ou);
@@ -462,11 +468,11 @@ PLORA_API int plora_swiglu_fwd(void* stream, int64_t n, const void* g, const voi
 }
 
 PLORA_API int plora_swiglu_bwd(void* stream, int64_t n, const void* da, const void* g, const void* u, void* dg,
-                               void* du) {
+                               void* du, void* act) {
   if (n % 8) return plora::set_error("swiglu: n must be a multiple of 8");
   swiglu_bwd_kernel<<<grid_for(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const bf16*>(da), static_cast<const bf16*>(g), static_cast<const bf16*>(u),
-      static_cast<bf16*>(dg), static_cast<bf16*>(du), n / 8);
+      static_cast<bf16*>(dg), static_cast<bf16*>(du), static_cast<bf16*>(act), n / 8);
   return launch_status("swiglu_bwd");
 }
 

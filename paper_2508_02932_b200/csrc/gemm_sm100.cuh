@@ -573,16 +573,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    // 8 warps: warp w drains TMEM lane quarter w%4, column half (w-2)/4, in 32-column
-    // chunks: TMEM -> registers (thread = row) -> bf16 -> per-warp smem staging (two
-    // 2 KB buffers, 64-byte swizzle, bank-conflict free) -> TMA bulk tensor store, or
-    // TMA reduce-add when accumulating into Y.  Stores are asynchronous, so TMEM is
-    // released as soon as the last chunk is in registers.  Warps whose 32 rows are only
-    // partly inside the tile (unaligned segments) fall back to masked direct stores.
+    // 8 warps: warp w drains TMEM lane quarter w%4, column half (w-2)/4, as 32-column
+    // chunks.  The first kDirect chunks go TMEM -> registers -> bf16 -> per-warp smem
+    // staging (two 2 KB buffers, 64-byte swizzle, bank-conflict free) -> TMA bulk tensor
+    // store (or TMA reduce-add when accumulating into Y); the remaining chunks are parked
+    // in registers (bf16-packed) so the accumulator is released after one TMEM pass and
+    // the next tile's mainloop overlaps the rest of the stores.  Warps whose 32 rows are
+    // only partly inside the tile (unaligned segments) use masked direct stores.
     const int ew = warp - 2;
     const int quarter = warp & 3;         // tcgen05.ld lane-quarter rule: warp w reads lanes 32*(w%4)..
     const int chalf = ew >> 2;
     constexpr int kChunks = Cfg::kBN / 32 / 2;   // chunks per warp
+    // chunks stored before the accumulator is released: all of them when the accumulator is
+    // double-buffered (NB = 1), otherwise park the rest in registers
+    constexpr int kDirect = Cfg::kAccStages > 1 ? kChunks : 3;
+    constexpr int kParked = kChunks - kDirect;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint8_t* stg = smem + S * Cfg::kStageBytes + 1024 + ew * 4096;   // 1024-B aligned (>= swizzle period)
     int acc = 0;
@@ -597,20 +602,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
       const int c0 = chalf * kChunks;
       const bool skip = (args.debug & 1) != 0;
-      uint32_t r[32];
-      if (!skip) tmem_ld_32x32b_x32(tb + c0 * 32, r);
-#pragma unroll 1
-      for (int j = 0; j < (skip ? 0 : kChunks); ++j) {
-        const int c = c0 + j;
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
-        if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c + 1) * 32, r);   // overlaps the stores below
-        const int col0 = t.n0 + c * 32;
-        if (col0 >= args.N || m_len <= 0 || (args.debug & 4)) continue;   // bit 2: TMEM drain only (experiment)
+      const bool store = !skip && !(args.debug & 4) && m_len > 0;   // bit 2: TMEM drain only (experiment)
+      // one chunk out of registers: staged TMA store for full 32-row warps, masked stores otherwise
+      auto emit = [&](int j, const uint32_t (&v)[16]) {
+        const int col0 = t.n0 + (c0 + j) * 32;
+        if (col0 >= args.N) return;
         if (m_len == 32) {
-          uint8_t* buf = stg + (j & 1) * 2048;
+          uint8_t* buf = stg + (issued & 1) * 2048;
           if (issued >= 2) {
             if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has read it
             __syncwarp();
@@ -618,7 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             *reinterpret_cast<uint4*>(buf + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) =
-                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -629,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
           ++issued;
         } else if (lane < m_len) {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(m0 + lane) * args.ldo;
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(pk);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int cc = col0 + 2 * q;
@@ -644,11 +642,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
             }
           }
         }
+      };
+      uint32_t pk[kParked > 0 ? kParked : 1][16];
+      if (!skip) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tb + c0 * 32, r);
+#pragma unroll
+        for (int j = 0; j < kChunks; ++j) {
+          tmem_ld_wait();
+          if (j < kDirect) {
+            uint32_t v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+            if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c0 + j + 1) * 32, r);   // overlaps the store below
+            if (store) emit(j, v);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              pk[j - kDirect][q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+            if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c0 + j + 1) * 32, r);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);   // accumulator free: next mainloop
       if (++acc == AS) { acc = 0; acc_phase ^= 1; }
+      if (!store) continue;
+#pragma unroll
+      for (int j = kDirect; j < kChunks; ++j) emit(j, pk[j - kDirect]);
     }
     if (lane == 0) bulk_wait<0>();   // all TMA stores complete before the CTA retires
     __syncwarp();

@@ -68,11 +68,15 @@ def swiglu_fwd(g: torch.Tensor, u: torch.Tensor, out: torch.Tensor | None = None
     return a
 
 
-def swiglu_bwd(da: torch.Tensor, g: torch.Tensor, u: torch.Tensor, out_g=None, out_u=None):
+def swiglu_bwd(da: torch.Tensor, g: torch.Tensor, u: torch.Tensor, out_g=None, out_u=None,
+               act_out: torch.Tensor | None = None):
+    """(dg, du) from da; dg/du may alias g/u.  act_out (optional) receives silu(g) * u,
+    bit-identical to swiglu_fwd, from the same pass."""
     dg = torch.empty_like(g) if out_g is None else out_g
     du = torch.empty_like(u) if out_u is None else out_u
     _lib.check(_lib.lib().plora_swiglu_bwd(_stream(), g.numel(), _need(da, "da"), _need(g, "g"), _need(u, "u"),
-                                           _need(dg, "dg"), _need(du, "du")), "swiglu_bwd")
+                                           _need(dg, "dg"), _need(du, "du"),
+                                           _need(act_out, "act_out", allow_none=True)), "swiglu_bwd")
     _LAUNCHES[0] += 1
     return dg, du
 

@@ -280,6 +280,15 @@ class PackedLoraTrainer:
         ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A"))              # dA (replicated)
         return dx
 
+    def _token_major(self, x: torch.Tensor) -> torch.Tensor:
+        """[B][H][s][hd]-shaped attention tensor -> [T][H*hd]: a free view when the
+        attention kernel already produced token-major memory, else one layout-change pass."""
+        B, H, s, hd = x.shape
+        xt = x.transpose(1, 2)
+        if xt.is_contiguous():
+            return xt.view(B * s, H * hd)
+        return ew.rope(xt, self.cos, self.sin, s, rotate=False)
+
     def _reduce(self, *ts):
         if self.tp is not None:
             for t in ts:
@@ -314,7 +323,7 @@ class PackedLoraTrainer:
         vg = v.view(B, s, KV, hd).transpose(1, 2).detach().requires_grad_()
         with torch.enable_grad():
             og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
-        attn = ew.rope(og.detach().transpose(1, 2), self.cos, self.sin, s, rotate=False)   # [T][H*hd]
+        attn = self._token_major(og.detach())                                           # [T][H*hd]
         o_out, hs_o = self._lin_fwd(layer, "o", attn, lw["o"])
         self._reduce(o_out, hs_o)                      # row-parallel (TP): Y and Hs are partial sums
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
@@ -335,13 +344,20 @@ class PackedLoraTrainer:
         cfg, lw = self.cfg, self.base.layers[layer]
         T, hd, H, KV, s = self.T, cfg.head_dim, self.H_l, self.KV_l, self.s
         B = T // s
-        # MLP: h_out = h_mid + down(swiglu(gate(x2), up(x2)))
-        act = ew.swiglu_fwd(sv.g, sv.u)                                   # recompute
-        d_act = self._lin_bwd(layer, "down", act, lw["down"], sv.hs["down"], dh)
-        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u)  # in place over g, u
+        # MLP: h_out = h_mid + down(swiglu(gate(x2), up(x2))).  The down projection's
+        # Cases 2/1/4 run first; the SwiGLU backward re-emits the activation in the same
+        # pass (no separate recompute), then Case 3 dA_down = act^T dH.
+        bank, meta = self.bank, self.meta
+        dh_down = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
+        ops.shrink(meta, dh, bank.shadow_of(layer, "down", "B"), dh_down)                     # K4
+        ops.segred(meta, dh, sv.hs["down"], bank.region_flat(bank.G, layer, "down", "B"))    # K3
+        d_act = ops.linear_expand(meta, dh, lw["down"], False, bank.shadow_of(layer, "down", "A"), dh_down)  # K6
+        act = torch.empty_like(sv.g)
+        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u, act_out=act)  # in place over g, u
         del d_act
+        ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
+        del act, dh_down
         x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
-        del act
         dx2 = self._lin_bwd_col(layer, "up", x2, lw["up"], sv.hs["up"], du)
         dx2 = self._lin_bwd_col(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
         self._reduce(dx2)
@@ -354,7 +370,7 @@ class PackedLoraTrainer:
         del d_attn
         dq = ew.rope(dq.transpose(1, 2), self.cos, self.sin, s, inverse=True)      # [T][H*hd]
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
-        dv = ew.rope(dv.transpose(1, 2), self.cos, self.sin, s, rotate=False)
+        dv = self._token_major(dv)
         x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
         dx1 = self._lin_bwd_col(layer, "v", x1, lw["v"], sv.hs["v"], dv, need_dx=need_dx)
         dx1 = self._lin_bwd_col(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1,

@@ -49,6 +49,12 @@ def test_swiglu():
     dg, du = ew.swiglu_bwd(da, g, u)
     rg, ru = ew.ref_swiglu_bwd(da, g, u)
     assert rel(dg, rg) < 4e-3 and rel(du, ru) < 4e-3
+    # fused variant: in place over g/u, re-emits the activation bit-identically
+    a_fwd = ew.swiglu_fwd(g, u)
+    g2, u2, act = g.clone(), u.clone(), torch.empty_like(g)
+    dg2, du2 = ew.swiglu_bwd(da, g2, u2, out_g=g2, out_u=u2, act_out=act)
+    assert torch.equal(act, a_fwd)
+    assert torch.equal(dg2, dg) and torch.equal(du2, du)
 
 
 def test_rope_and_layout():
