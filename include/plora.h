@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 3
+#define PLORA_ABI_VERSION 4
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -66,6 +66,8 @@ typedef struct plora_pack {
   int32_t n_ptiles;        /* entries in d_ptiles */
   int32_t pad_;
   const int32_t* d_ptiles; /* [n_ptiles][4] = {m0, m_len (1..256), adapter, 0}: CTA-pair tiles */
+  const int64_t* h_row_off;/* [n+1] HOST copy of the row offsets (may be NULL): lets the
+                              segment reductions balance their tiles across SMs (LPT) */
 } plora_pack_t;
 
 /* Library / error plumbing. */
@@ -122,6 +124,17 @@ PLORA_API int plora_lora_shrink(void* stream, const plora_pack_t* pack, int64_t 
  * written into the adapter-major region G (P bf16 [T][Mdim], Q bf16 [T][rpad64]). */
 PLORA_API int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t Mdim,
                      const void* P, const void* Q, float* G);
+
+/* Multi-target K2a / K5 for n_multi (1..3) targets that share their input P (the
+ * normed layer input of q/k/v, or of gate/up): P is read ONCE for all targets.
+ *   shrink_multi : outs[j][T][rpad64] = alpha_i * P_i L_sh[j]_i
+ *   segred_multi : G[j] (f32 region) = P_i^T Q[j]_i per segment
+ * L_sh / outs / Q / G are host arrays of n_multi device pointers.  With ranks > 64
+ * (nb > 1) they fall back to one launch per target. */
+PLORA_API int plora_lora_shrink_multi(void* stream, const plora_pack_t* pack, int64_t K,
+                     const void* P, int32_t n_multi, const void* const* L_sh, void* const* outs);
+PLORA_API int plora_lora_segred_multi(void* stream, const plora_pack_t* pack, int64_t Mdim,
+                     const void* P, int32_t n_multi, const void* const* Q, float* const* G);
 
 /* K1 + K2b only: Y = X op(W) + Hs_i B_i (+ residual) with a caller-provided Hs
  * (e.g. saved from an earlier shrink, or perturbed by a gradient checker). */

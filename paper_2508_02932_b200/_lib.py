@@ -27,6 +27,8 @@ EXPORTS = (
     "plora_linear_fwd",
     "plora_lora_shrink",
     "plora_lora_segred",
+    "plora_lora_shrink_multi",
+    "plora_lora_segred_multi",
     "plora_linear_expand",
     "plora_linear_bwd",
     "plora_adamw",
@@ -41,7 +43,7 @@ EXPORTS = (
     "plora_ce_apply",
 )
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class PloraError(RuntimeError):
@@ -65,6 +67,7 @@ class PackStruct(ctypes.Structure):
         ("n_ptiles", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
         ("d_ptiles", ctypes.c_void_p),
+        ("h_row_off", ctypes.c_void_p),
     ]
 
 
@@ -90,6 +93,10 @@ _SIGNATURES = {
                           _vp, _vp, _i64, _vp], ctypes.c_int),
     "plora_lora_shrink": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_lora_segred": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp], ctypes.c_int),
+    "plora_lora_shrink_multi": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _i32, ctypes.POINTER(_vp),
+                                 ctypes.POINTER(_vp)], ctypes.c_int),
+    "plora_lora_segred_multi": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _i32, ctypes.POINTER(_vp),
+                                 ctypes.POINTER(_vp)], ctypes.c_int),
     "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                              _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_bwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,

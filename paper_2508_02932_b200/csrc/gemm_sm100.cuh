@@ -50,6 +50,14 @@ struct __align__(64) GemmArgs {
   int32_t nb;        // 64-column rank blocks
   int32_t debug;     // bit 0: skip epilogue stores (profiling experiments only)
   int32_t accumulate;  // pair kernel: Y += result (TMA reduce-add) instead of Y = result
+  // Multi-target SHRINK / SEGRED (n_multi > 1, rank <= 64): targets j = 0..n_multi-1 share
+  // the A operand (the same X), each with its own 64-column B operand (tmB, tmB2, tmB3)
+  // and output (out, out2, out3); BN = 64 * n_multi and column chunk c belongs to target c/2.
+  int32_t n_multi;
+  CUtensorMap tmB2;
+  CUtensorMap tmB3;
+  void* out2;
+  void* out3;
 };
 
 constexpr int kBM = 128;
@@ -62,13 +70,49 @@ struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;              // 16 KB
   static constexpr int kBBytes = BN * kBK * 2;               // BN x 64 bf16
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kStages = (BN == 256) ? 4 : (BN == 192 ? 5 : (BN == 128 ? 6 : 8));
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 :
+                                   (2 * BN <= 256 ? 256 : 512)));   // power of two >= 2 accumulators
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TileInfo {
   int m0, m_len, adapter, k0, k_len, n0, n_main, n_lora, rank;
+};
+
+// Static longest-processing-time-first schedule for the segment reductions (K3/K5):
+// their tiles cost ~T_i (the adapter's token count), which varies 4x across a pack,
+// so round-robin tile assignment leaves some SMs with 1.5x the mean work.  The host
+// computes the LPT assignment (plora_abi.cu) and passes it in kernel parameter space:
+// CTA b runs tiles[off[b] .. off[b+1]).
+constexpr int kSchedMaxCtas = 160;
+constexpr int kSchedMaxTiles = 6144;
+struct SegSched {
+  int32_t n_ctas;
+  uint16_t off[kSchedMaxCtas + 1];
+  uint16_t tiles[kSchedMaxTiles];
+};
+
+// The persistent tile loop shared by the three warp roles.
+struct TileIter {
+  int j, end, step;
+  const uint16_t* list;
+  __device__ __forceinline__ TileIter(const SegSched* sched, int total) {
+    if (sched != nullptr) {
+      j = sched->off[blockIdx.x];
+      end = sched->off[blockIdx.x + 1];
+      step = 1;
+      list = sched->tiles;
+    } else {
+      j = blockIdx.x;
+      end = total;
+      step = gridDim.x;
+      list = nullptr;
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return j < end; }
+  __device__ __forceinline__ int tile() const { return list ? static_cast<int>(list[j]) : j; }
+  __device__ __forceinline__ void next() { j += step; }
 };
 
 template <int BN, int MODE>
@@ -120,7 +164,7 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& a, int idx) {
 }
 
 template <int BN, int MODE, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_constant__ GemmArgs args) {
+__device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* sched) {
   using Cfg = GemmCfg<BN>;
   constexpr bool A_MN = (MODE == MODE_SEGRED);
   constexpr bool MAIN_B_MN = (MODE == MODE_GEMM) ? B_MN : true;
@@ -166,8 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const TileInfo t = decode_tile<BN, MODE>(args, idx);
+      for (TileIter it(sched, total); it.valid(); it.next()) {
+        const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
         const int nblk = t.n_main + t.n_lora;
         for (int b = 0; b < nblk; ++b) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -182,7 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
             } else {
               tma_load_2d(sA, &args.tmA, &full_bar[stage], kc, t.m0);
             }
-            if (MODE == MODE_SHRINK) {
+            if (MODE != MODE_GEMM && args.n_multi > 1) {   // one 64-column B chunk per target
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) {
+                const CUtensorMap* mj = j == 0 ? &args.tmB : (j == 1 ? &args.tmB2 : &args.tmB3);
+                if (MODE == MODE_SHRINK) tma_load_3d(sB + j * 8192, mj, &full_bar[stage], 0, kc, t.adapter);
+                else                     tma_load_2d(sB + j * 8192, mj, &full_bar[stage], 0, kc);
+              }
+            } else if (MODE == MODE_SHRINK) {
               tma_load_3d(sB, &args.tmB, &full_bar[stage], t.n0, kc, t.adapter);
             } else if (MAIN_B_MN) {
 #pragma unroll
@@ -208,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-      const TileInfo t = decode_tile<BN, MODE>(args, idx);
+    for (TileIter it(sched, total); it.valid(); it.next()) {
+      const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
       const int nblk = t.n_main + t.n_lora;
       if (nblk == 0) continue;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -228,10 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
           if (valid < kBK) {
             const int nrows = kBK - valid;
             const int per = nrows * 8;  // 16-byte chunks per sub-tile
-            for (int i = lane; i < 3 * per; i += 32) {
+            for (int i = lane; i < (2 + BN / 64) * per; i += 32) {
               const int sub = i / per;
               const int rem = i - sub * per;
-              uint8_t* base = (sub < 2) ? (sA + sub * 8192) : sB;
+              uint8_t* base = (sub < 2) ? (sA + sub * 8192) : sB + (sub - 2) * 8192;
               reinterpret_cast<uint4*>(base + (valid + rem / 8) * 128)[rem % 8] = make_uint4(0, 0, 0, 0);
             }
             fence_proxy_async_smem();
@@ -266,19 +317,25 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-      const TileInfo t = decode_tile<BN, MODE>(args, idx);
+    for (TileIter it(sched, total); it.valid(); it.next()) {
+      const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
       const int nblk = t.n_main + t.n_lora;
       if (MODE == MODE_SEGRED) {
         const int ld = args.rpad_off[t.adapter + 1] - args.rpad_off[t.adapter];
-        float* g = reinterpret_cast<float*>(args.out) +
-                   static_cast<int64_t>(args.M) * args.rpad_off[t.adapter];
+        const int64_t goff = static_cast<int64_t>(args.M) * args.rpad_off[t.adapter] +
+                             static_cast<int64_t>(t.m0 + row) * ld;
+        const bool multi = args.n_multi > 1;
         const bool row_ok = row < t.m_len;
-        float* grow = g + static_cast<int64_t>(t.m0 + row) * ld;
         if (nblk == 0) {
-          if (row_ok)
-            for (int c = t.n0; c < min(t.n0 + BN, ld); c += 4)
-              *reinterpret_cast<float4*>(grow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row_ok) {
+            for (int j = 0; j < (multi ? args.n_multi : 1); ++j) {
+              float* grow = reinterpret_cast<float*>(j == 0 ? args.out : (j == 1 ? args.out2 : args.out3)) + goff;
+              const int c_lo = multi ? 0 : t.n0;
+              const int c_hi = multi ? min(64, ld) : min(t.n0 + BN, ld);
+              for (int c = c_lo; c < c_hi; c += 4)
+                *reinterpret_cast<float4*>(grow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
           continue;
         }
         mbar_wait(&tfull_bar[acc], acc_phase);
@@ -289,7 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
           uint32_t r[32];
           tmem_ld_32x32b_x32(tb + c * 32, r);
           tmem_ld_wait();
-          const int col0 = t.n0 + c * 32;
+          const int tg = multi ? (c >> 1) : 0;
+          float* grow = reinterpret_cast<float*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) + goff;
+          const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
           if (row_ok) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
@@ -307,14 +366,17 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
         const float scale = (MODE == MODE_SHRINK) ? args.alpha[t.adapter] : 1.0f;
         const bool row_ok = row < t.m_len;
         const int64_t orow = static_cast<int64_t>(t.m0 + row) * args.ldo;
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow;
+        const bool multi = MODE == MODE_SHRINK && args.n_multi > 1;
         const __nv_bfloat16* res = (MODE == MODE_GEMM && args.residual) ? args.residual + orow : nullptr;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tb + c * 32, r);
           tmem_ld_wait();
-          const int col0 = t.n0 + c * 32;
+          const int tg = multi ? (c >> 1) : 0;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) +
+                             orow;
+          const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
           if (row_ok && col0 < args.N) {
             float v[32];
 #pragma unroll
@@ -368,6 +430,18 @@ __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_co
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
+}
+
+template <int BN, int MODE, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_constant__ GemmArgs args) {
+  gemm_body<BN, MODE, B_MN>(args, nullptr);
+}
+
+// Segment reduction with a host-computed LPT tile schedule (see SegSched).
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __grid_constant__ GemmArgs args,
+                                                                        const __grid_constant__ SegSched sched) {
+  gemm_body<BN, MODE_SEGRED, true>(args, &sched);
 }
 
 // ============================================================================

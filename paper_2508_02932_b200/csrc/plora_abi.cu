@@ -10,7 +10,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <memory>
 #include <mutex>
+#include <queue>
+#include <unordered_map>
+#include <vector>
 #include <string>
 
 #include "../../include/plora.h"
@@ -289,6 +294,81 @@ static int run_shrink(cudaStream_t st, const plora_pack_t* pack, int64_t K, cons
   return launch<64, MODE_SHRINK, true>(a, st);
 }
 
+static bool g_segred_lpt = [] {
+  const char* e = getenv("PLORA_SEGRED_LPT");
+  return !(e && e[0] == '0');
+}();
+
+// LPT schedule for the segment reductions: tile (adapter a, m-tile, n-tile) costs
+// ceil(T_a / 64) K-blocks + a fixed epilogue/fill overhead; tiles are taken in
+// decreasing cost and each goes to the least-loaded CTA (list scheduling in LPT order,
+// within 4/3 of optimal).  Schedules are cached per (row offsets, tile grid, SM count).
+static bool segred_schedule(const plora_pack_t* pack, int mt_per, int n_ntiles, SegSched* dst) {
+  const int n = pack->n_adapters;
+  const int per = mt_per * n_ntiles;
+  const int64_t total = static_cast<int64_t>(n) * per;
+  const int sms = num_sms();
+  if (total <= 0 || total > kSchedMaxTiles || sms > kSchedMaxCtas) return false;
+  uint64_t h = 1469598103934665603ull;
+  for (int i = 0; i <= n; ++i) h = (h ^ static_cast<uint64_t>(pack->h_row_off[i])) * 1099511628211ull;
+  h = (h ^ static_cast<uint64_t>(n)) * 1099511628211ull;
+  const uint64_t key = h ^ (static_cast<uint64_t>(mt_per) << 40) ^ (static_cast<uint64_t>(n_ntiles) << 52) ^
+                       static_cast<uint64_t>(sms);
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, std::unique_ptr<SegSched>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    memcpy(dst, it->second.get(), sizeof(SegSched));   // copied under the lock: entries may be evicted
+    return true;
+  }
+  const int ctas = static_cast<int>(total < sms ? total : sms);
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  auto cost = [&](int a) { return (pack->h_row_off[a + 1] - pack->h_row_off[a] + 63) / 64 + 3; };
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+  std::vector<std::vector<uint16_t>> lists(ctas);
+  using Slot = std::pair<int64_t, int>;   // (load, cta)
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  for (int c = 0; c < ctas; ++c) heap.push({0, c});
+  for (int a : order) {
+    const int64_t w = cost(a);
+    for (int t = 0; t < per; ++t) {
+      Slot s = heap.top();
+      heap.pop();
+      lists[s.second].push_back(static_cast<uint16_t>(a * per + t));
+      heap.push({s.first + w, s.second});
+    }
+  }
+  auto sched = std::make_unique<SegSched>();
+  memset(sched.get(), 0, sizeof(SegSched));
+  sched->n_ctas = ctas;
+  int pos = 0;
+  for (int c = 0; c < ctas; ++c) {
+    sched->off[c] = static_cast<uint16_t>(pos);
+    for (uint16_t t : lists[c]) sched->tiles[pos++] = t;
+  }
+  sched->off[ctas] = static_cast<uint16_t>(pos);
+  memcpy(dst, sched.get(), sizeof(SegSched));
+  if (cache.size() >= 256) cache.clear();
+  cache.emplace(key, std::move(sched));
+  return true;
+}
+
+template <int BN>
+static int launch_segred_lpt(const GemmArgs& args, const SegSched& sched, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = plora_segred_lpt_kernel<BN>;
+  static bool configured = false;
+  if (!configured) {
+    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    configured = true;
+  }
+  kern<<<sched.n_ctas, kThreads, Cfg::kSmemBytes, stream>>>(args, sched);
+  PLORA_CUDA(cudaGetLastError());
+  return 0;
+}
+
 // Segment reduction: G_i[Mdim][rpad16_i] = P_i^T Q_i over the tokens of segment i.
 //   P: [T][Mdim] bf16, Q: [T][64nb] bf16, G: f32 adapter-major region.
 static int run_segred(cudaStream_t st, const plora_pack_t* pack, int64_t Mdim, const void* P,
@@ -311,7 +391,73 @@ static int run_segred(cudaStream_t st, const plora_pack_t* pack, int64_t Mdim, c
   a.M = static_cast<int>(Mdim);
   a.N = static_cast<int>(R64);
   a.out = G;
+  if (pack->h_row_off != nullptr && g_segred_lpt) {
+    SegSched sched;
+    if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched)) return launch_segred_lpt<64>(a, sched, st);
+  }
   return launch<64, MODE_SEGRED, true>(a, st);
+}
+
+// Multi-target shrink: out_j[T][64] = alpha_i * P[T][K] * L_j,i[K][64] for n_multi targets
+// that share P (q/k/v or gate/up): P is read once.  Requires nb == 1 (ranks <= 64).
+static int run_shrink_multi(cudaStream_t st, const plora_pack_t* pack, int64_t K, const void* P, int n_multi,
+                            const void* const* L, void* const* out) {
+  const int64_t T = pack->total_tokens;
+  if (T <= 0 || pack->n_mtiles == 0) return 0;
+  if (K % 8) return fail("shrink: K must be a multiple of 8");
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc;
+  if ((rc = make_map_2d(&a.tmA, P, K, T, K, 64, kBM))) return rc;
+  CUtensorMap* maps[3] = {&a.tmB, &a.tmB2, &a.tmB3};
+  for (int j = 0; j < n_multi; ++j)
+    if ((rc = make_map_3d(maps[j], L[j], 64, K, pack->n_adapters, 64, 64))) return rc;
+  a.mtiles = pack->d_mtiles;
+  a.alpha = pack->d_alpha;
+  a.n_groups = pack->n_mtiles;
+  a.n_ntiles = 1;
+  a.M = static_cast<int>(T);
+  a.N = 64;
+  a.K = static_cast<int>(K);
+  a.out = out[0];
+  a.out2 = n_multi > 1 ? out[1] : nullptr;
+  a.out3 = n_multi > 2 ? out[2] : nullptr;
+  a.ldo = 64;
+  a.n_multi = n_multi;
+  return n_multi == 3 ? launch<192, MODE_SHRINK, true>(a, st) : launch<128, MODE_SHRINK, true>(a, st);
+}
+
+// Multi-target segment reduction: G_j,i[Mdim][rpad16_i] = P_i^T Q_j,i for n_multi targets
+// sharing P (the layer input X of q/k/v or gate/up).  Requires nb == 1.
+static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t Mdim, const void* P, int n_multi,
+                            const void* const* Q, float* const* G) {
+  const int64_t T = pack->total_tokens;
+  if (Mdim % 8) return fail("segment reduction: Mdim must be a multiple of 8");
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc;
+  const int64_t Tm = T > 0 ? T : 1;
+  if ((rc = make_map_2d(&a.tmA, P, Mdim, Tm, Mdim, 64, 64))) return rc;
+  CUtensorMap* maps[3] = {&a.tmB, &a.tmB2, &a.tmB3};
+  for (int j = 0; j < n_multi; ++j)
+    if ((rc = make_map_2d(maps[j], Q[j], 64, Tm, 64, 64, 64))) return rc;
+  a.row_off = pack->d_row_off;
+  a.rpad_off = pack->d_rpad_off;
+  a.mt_per = static_cast<int>((Mdim + kBM - 1) / kBM);
+  a.n_groups = pack->n_adapters * a.mt_per;
+  a.n_ntiles = 1;
+  a.M = static_cast<int>(Mdim);
+  a.N = 64;
+  a.out = G[0];
+  a.out2 = n_multi > 1 ? G[1] : nullptr;
+  a.out3 = n_multi > 2 ? G[2] : nullptr;
+  a.n_multi = n_multi;
+  if (pack->h_row_off != nullptr && g_segred_lpt) {
+    SegSched sched;
+    if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched))
+      return n_multi == 3 ? launch_segred_lpt<192>(a, sched, st) : launch_segred_lpt<128>(a, sched, st);
+  }
+  return n_multi == 3 ? launch<192, MODE_SEGRED, true>(a, st) : launch<128, MODE_SEGRED, true>(a, st);
 }
 
 }  // namespace plora
@@ -377,6 +523,34 @@ int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t Mdim, cons
   if ((rc = check_pack(pack))) return rc;
   if (!G) return fail("segred: output region is NULL");
   return run_segred(static_cast<cudaStream_t>(stream), pack, Mdim, P, Q, G);
+}
+
+int plora_lora_shrink_multi(void* stream, const plora_pack_t* pack, int64_t K, const void* P, int32_t n_multi,
+                            const void* const* L_sh, void* const* outs) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (n_multi < 1 || n_multi > 3) return fail("shrink_multi: n_multi must be 1..3");
+  if (pack->nb != 1 || n_multi == 1) {   // ranks > 64: one launch per target
+    for (int j = 0; j < n_multi; ++j)
+      if ((rc = run_shrink(static_cast<cudaStream_t>(stream), pack, K, P, L_sh[j], outs[j]))) return rc;
+    return 0;
+  }
+  return run_shrink_multi(static_cast<cudaStream_t>(stream), pack, K, P, n_multi, L_sh, outs);
+}
+
+int plora_lora_segred_multi(void* stream, const plora_pack_t* pack, int64_t Mdim, const void* P, int32_t n_multi,
+                            const void* const* Q, float* const* G) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (n_multi < 1 || n_multi > 3) return fail("segred_multi: n_multi must be 1..3");
+  for (int j = 0; j < n_multi; ++j)
+    if (!G[j]) return fail("segred_multi: output region is NULL");
+  if (pack->nb != 1 || n_multi == 1) {
+    for (int j = 0; j < n_multi; ++j)
+      if ((rc = run_segred(static_cast<cudaStream_t>(stream), pack, Mdim, P, Q[j], G[j]))) return rc;
+    return 0;
+  }
+  return run_segred_multi(static_cast<cudaStream_t>(stream), pack, Mdim, P, n_multi, Q, G);
 }
 
 int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int64_t k,

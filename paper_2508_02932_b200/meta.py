@@ -85,6 +85,8 @@ class PackMeta:
         s.d_alpha = dev["alpha"].data_ptr()
         s.n_ptiles = int(self.ptiles.shape[0])
         s.d_ptiles = dev["ptiles"].data_ptr() if s.n_ptiles else None
+        self._h_row_off = np.ascontiguousarray(self.row_offsets, dtype=np.int64)   # kept alive with the struct
+        s.h_row_off = self._h_row_off.ctypes.data
         self._dev = dev
         self._struct = s
         self.device = device

@@ -262,22 +262,34 @@ class PackedLoraTrainer:
                               bank.region_flat(bank.G, layer, tname, "B"),
                               dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
 
-    def _lin_bwd_col(self, layer: int, tname: str, x, w, hs, dy, dx_residual=None, dx_out=None, need_dx=True):
-        """Column-parallel backward under TP: dH_s is partial, so dA needs the
-        all-reduced dH (tp.py); dB_s and the partial dX_s are local."""
-        if self.tp is None:
-            return self._lin_bwd(layer, tname, x, w, hs, dy, need_dx=need_dx, dx_residual=dx_residual,
-                                 dx_out=dx_out)
-        bank, meta = self.bank, self.meta
-        dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
-        ops.shrink(meta, dy, bank.shadow_of(layer, tname, "B"), dh)                       # partial dH_s
-        ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, tname, "B"))             # dB_s (local)
+    def _group_fwd(self, layer: int, names, x: torch.Tensor):
+        """Forward of targets sharing the input x (q/k/v or gate/up): ONE K2a launch reads
+        x once for every target's Hs, then per target the K1 GEMM with K2b fused."""
+        bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
+        hss = [torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device) for _ in names]
+        ops.shrink_multi(meta, x, [bank.shadow_of(layer, nm, "A") for nm in names], hss)
+        ys = [ops.linear_expand(meta, x, lw[nm], True, bank.shadow_of(layer, nm, "B"), hs)
+              for nm, hs in zip(names, hss)]
+        return ys, hss
+
+    def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
+        """Backward of targets sharing the input x: per target K4 dH, K3 dB and the K6 dX
+        GEMM accumulated into one input gradient; then ONE K5 launch for every dA
+        (x read once).  Column-parallel under TP: dH_s and dX_s are partial, dH is
+        all-reduced before dA (tp.py), dX by the caller."""
+        bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
         dx = None
-        if need_dx:
-            dx = ops.linear_expand(meta, dy, w, False, bank.shadow_of(layer, tname, "A"), dh,  # partial dX_s
-                                   dx_out, dx_residual)
-        self.tp.all_reduce_(dh)
-        ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A"))              # dA (replicated)
+        dhs = []
+        for nm, hs, dy in zip(names, hss, dys):
+            dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
+            ops.shrink(meta, dy, bank.shadow_of(layer, nm, "B"), dh)                        # K4 (Case 2)
+            ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, nm, "B"))              # K3 (Case 1)
+            if need_dx:                                                                     # K6 (Case 4)
+                dx = ops.linear_expand(meta, dy, lw[nm], False, bank.shadow_of(layer, nm, "A"), dh,
+                                       y_out=dx, residual=dx)
+            dhs.append(dh)
+        self._reduce(*dhs)
+        ops.segred_multi(meta, x, dhs, [bank.region_flat(bank.G, layer, nm, "A") for nm in names])  # K5
         return dx
 
     def _token_major(self, x: torch.Tensor) -> torch.Tensor:
@@ -308,9 +320,7 @@ class PackedLoraTrainer:
             x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
         else:
             h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
-        q, hs_q = self._lin_fwd(layer, "q", x1, lw["q"])
-        k, hs_k = self._lin_fwd(layer, "k", x1, lw["k"])
-        v, hs_v = self._lin_fwd(layer, "v", x1, lw["v"])
+        (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1)
         del x1
         if cfg.qkv_bias:
             q += lw["q_bias"]
@@ -328,8 +338,7 @@ class PackedLoraTrainer:
         self._reduce(o_out, hs_o)                      # row-parallel (TP): Y and Hs are partial sums
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
-        g, hs_g = self._lin_fwd(layer, "gate", x2, lw["gate"])
-        u, hs_u = self._lin_fwd(layer, "up", x2, lw["up"])
+        (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2)
         del x2
         act = ew.swiglu_fwd(g, u)
         d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
@@ -358,8 +367,7 @@ class PackedLoraTrainer:
         ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
         del act, dh_down
         x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
-        dx2 = self._lin_bwd_col(layer, "up", x2, lw["up"], sv.hs["up"], du)
-        dx2 = self._lin_bwd_col(layer, "gate", x2, lw["gate"], sv.hs["gate"], dg, dx_residual=dx2, dx_out=dx2)
+        dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))
         self._reduce(dx2)
         del dg, du, x2
         d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh, out=dx2)
@@ -372,11 +380,8 @@ class PackedLoraTrainer:
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
         dv = self._token_major(dv)
         x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
-        dx1 = self._lin_bwd_col(layer, "v", x1, lw["v"], sv.hs["v"], dv, need_dx=need_dx)
-        dx1 = self._lin_bwd_col(layer, "k", x1, lw["k"], sv.hs["k"], dk, dx_residual=dx1, dx_out=dx1,
-                                need_dx=need_dx)
-        dx1 = self._lin_bwd_col(layer, "q", x1, lw["q"], sv.hs["q"], dq, dx_residual=dx1, dx_out=dx1,
-                                need_dx=need_dx)
+        dx1 = self._group_bwd(layer, ("v", "k", "q"), x1, (sv.hs["v"], sv.hs["k"], sv.hs["q"]), (dv, dk, dq),
+                              need_dx=need_dx)
         del dq, dk, dv, x1
         if not need_dx:   # first layer: the embedding is frozen, no input gradient
             return None

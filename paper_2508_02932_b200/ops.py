@@ -160,6 +160,44 @@ def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) ->
     return g
 
 
+def _ptr_array(ts, name, dtype=torch.bfloat16):
+    arr = (ctypes.c_void_p * len(ts))(*[_need(t, f"{name}[{j}]", dtype) for j, t in enumerate(ts)])
+    return ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), arr
+
+
+def shrink_multi(meta: PackMeta, p: torch.Tensor, l_shs, outs) -> list:
+    """K2a for targets sharing the input p (q/k/v or gate/up): outs[j] = alpha_i p_i L_j,i,
+    p read once (one launch when every rank <= 64)."""
+    T, K = p.shape
+    t = _TIMER.start() if _TIMER else None
+    lp, _k1 = _ptr_array(l_shs, "l_sh")
+    op, _k2 = _ptr_array(outs, "out")
+    _lib.check(_lib.lib().plora_lora_shrink_multi(_stream(), ctypes.byref(meta.struct), K, _need(p, "p"),
+                                                  len(outs), lp, op), "plora_lora_shrink_multi")
+    _LAUNCHES[0] += 1 if meta.nb == 1 else len(outs)
+    if t is not None:
+        tr, R = _lora_work(meta)
+        m = len(outs)
+        _TIMER.stop("shrink", t, flops=2.0 * K * tr * m, nbytes=2.0 * T * K + m * (2.0 * K * R + 2.0 * tr))
+    return outs
+
+
+def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
+    """K5 for targets sharing p: G_j,i = p_i^T Q_j,i (fp32, adapter-major regions), p read once."""
+    T, Mdim = p.shape
+    t = _TIMER.start() if _TIMER else None
+    qp, _k1 = _ptr_array(qs, "q")
+    gp, _k2 = _ptr_array(gs, "g", torch.float32)
+    _lib.check(_lib.lib().plora_lora_segred_multi(_stream(), ctypes.byref(meta.struct), Mdim, _need(p, "p"),
+                                                  len(gs), qp, gp), "plora_lora_segred_multi")
+    _LAUNCHES[0] += 1 if meta.nb == 1 else len(gs)
+    if t is not None:
+        tr, R = _lora_work(meta)
+        m = len(gs)
+        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr * m, nbytes=2.0 * T * Mdim + m * (2.0 * tr + 4.0 * Mdim * R))
+    return gs
+
+
 def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
                   bt_sh: torch.Tensor, hs: torch.Tensor, y_out: torch.Tensor | None = None,
                   residual: torch.Tensor | None = None) -> torch.Tensor:

@@ -143,3 +143,58 @@ def test_deterministic_grads():
         outs.append((y, dx, ga, gb))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_segred_lpt_schedule_matches_round_robin():
+    """The LPT tile schedule (host row offsets present) and plain round-robin give
+    bit-identical segment reductions: each output tile is still owned by one CTA."""
+    ranks = [8, 64, 16, 32, 8, 64, 1, 48]
+    tokens = [4096, 1024, 0, 2048, 333, 1024, 4096, 1500]
+    for mdim in (4096, 1024, 14336):
+        meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, mdim, 256, seed=3)
+        q = (torch.randn(meta.total_tokens, meta.rpad64, device="cuda") * 0.1).to(bf)
+        g_lpt = torch.full((mdim * meta.rpad16_total,), float("nan"), device="cuda")
+        g_rr = torch.full_like(g_lpt, float("nan"))
+        ops.segred(meta, x, q, g_lpt)
+        saved = meta.struct.h_row_off
+        meta.struct.h_row_off = None            # no host offsets -> round-robin schedule
+        try:
+            ops.segred(meta, x, q, g_rr)
+        finally:
+            meta.struct.h_row_off = saved
+        torch.cuda.synchronize()
+        assert not torch.isnan(g_lpt).any()
+        assert torch.equal(g_lpt, g_rr)
+        # and against the fp32 reference
+        for i in range(meta.n_adapters):
+            s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+            rp = int(meta.rpad_off[i + 1] - meta.rpad_off[i])
+            blk = g_lpt[mdim * int(meta.rpad_off[i]): mdim * int(meta.rpad_off[i + 1])].view(mdim, rp)
+            ref = x[s:e].float().t() @ q[s:e, :rp].float()
+            assert rel(blk, ref) < 1e-4 if e > s else torch.equal(blk, torch.zeros_like(blk))
+
+
+@pytest.mark.parametrize("n_multi", [2, 3])
+def test_multi_target_shrink_and_segred_match_single(n_multi):
+    """K2a / K5 over targets sharing their input (q/k/v, gate/up) in one launch equal the
+    per-target launches bit for bit (same K order per output column)."""
+    ranks = [8, 64, 16, 32, 8, 64, 1, 48]
+    tokens = [4096, 1024, 0, 2048, 333, 1024, 4096, 1500]
+    d = 4096
+    meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, 256, seed=5)
+    T, R64 = meta.total_tokens, meta.rpad64
+    g = torch.Generator(device="cuda").manual_seed(9)
+    ls = [(torch.randn(meta.n_adapters, d, R64, device="cuda", generator=g) * 0.02).to(bf) for _ in range(n_multi)]
+    outs = [torch.empty(T, R64, device="cuda", dtype=bf) for _ in range(n_multi)]
+    ops.shrink_multi(meta, x, ls, outs)
+    for l, o in zip(ls, outs):
+        ref = torch.empty_like(o)
+        ops.shrink(meta, x, l, ref)
+        assert torch.equal(o, ref)
+    qs = [(torch.randn(T, R64, device="cuda", generator=g) * 0.1).to(bf) for _ in range(n_multi)]
+    gs = [torch.full((d * meta.rpad16_total,), float("nan"), device="cuda") for _ in range(n_multi)]
+    ops.segred_multi(meta, x, qs, gs)
+    for q, gm in zip(qs, gs):
+        ref = torch.full_like(gm, float("nan"))
+        ops.segred(meta, x, q, ref)
+        assert torch.equal(gm, ref)
