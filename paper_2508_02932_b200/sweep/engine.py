@@ -8,11 +8,13 @@ SPEC.md:550) closes the planner loop:
   member's train_steps -> measured per-job times and ProfileRecords -> a B200
   calibrated TimeModel (calibrate_time_model) -> re-plan / report makespan.
 
-Multi-GPU: jobs are independent, so ranks never exchange data; the only
-collective is the final max-reduction of the per-rank wall time (and the
-gather of job records) over torch.distributed (NCCL on the box, gloo in the
-CPU tests).  Jobs of degree > 1 would need the tensor-parallel path (C4), which
-is not built yet: ``execute`` refuses them.
+Multi-GPU: jobs are independent, so ranks never exchange data between jobs; the
+collectives are the final gather of job records / per-device busy time over
+torch.distributed (NCCL on the box, gloo in the CPU tests) and, inside a job of
+degree d > 1, the tensor-parallel all-reduces of that job's d ranks (tp.py,
+config C4): ``execute`` creates one process group per distinct device set of the
+queue (every rank, same order), and each member rank trains its Megatron shard
+of the job.  TP jobs need one process per GPU (world == gpu_count).
 
 ``run_job`` is injectable so the host-side scheduling logic is testable without
 a GPU (tests/test_engine.py runs it under gloo, world size 2).
@@ -62,8 +64,9 @@ def _base(model_name: str, device: str):
 
 
 def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, steps_override: int | None = None,
-                     warmup: int = 1) -> tuple:
-    """Run one packed job on ``device``: returns (steps, seconds, mean iteration seconds, losses)."""
+                     warmup: int = 1, tp=None) -> tuple:
+    """Run one packed job on ``device`` (its TP shard when ``tp`` is a communicator over
+    the job's ranks): returns (steps, seconds, mean iteration seconds, losses)."""
     import torch
 
     from ..model import PRESETS, AdapterSpec, PackedLoraTrainer
@@ -71,8 +74,9 @@ def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, ste
     cfgs = [configs_by_id[c] for c in job.configs]
     seq = max(c.seq_len for c in cfgs)
     specs = [AdapterSpec(rank=c.rank, alpha=c.alpha, batch=c.batch_size, lr=c.learning_rate) for c in cfgs]
-    trainer = PackedLoraTrainer(PRESETS[model_name], specs, seq, device=device, base=_base(model_name, device),
-                                adapter_seeds=[int(hashlib.sha256(c.id.encode()).hexdigest()[:8], 16) for c in cfgs])
+    seeds = [int(hashlib.sha256(c.id.encode()).hexdigest()[:8], 16) for c in cfgs]
+    base = _base(model_name, device) if tp is None or tp.world == 1 else None   # TP shards: per-job base slices
+    trainer = PackedLoraTrainer(PRESETS[model_name], specs, seq, device=device, base=base, adapter_seeds=seeds, tp=tp)
     steps = steps_override or max(c.train_steps for c in cfgs)
     tokens = trainer.synthetic_tokens().to(device)
     for _ in range(warmup):
@@ -89,16 +93,40 @@ def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, ste
     return steps, dt, dt / steps, out
 
 
+def tp_groups(queue: JobQueue, placement: Placement, world: int, gpu_count: int,
+              new_group: Callable | None = None) -> dict:
+    """One communicator per distinct device set of the queue's degree > 1 jobs, created on
+    every rank in the same (sorted) order -- torch.distributed.new_group is collective."""
+    sets = sorted({placement.devices[j.id] for j in queue.jobs() if j.degree > 1})
+    if not sets:
+        return {}
+    if world != gpu_count:
+        raise NotImplementedError("tensor-parallel jobs need one process per GPU (world == gpu_count)")
+    if new_group is None:
+        import torch.distributed as dist
+
+        from ..tp import DistComm
+
+        def new_group(ranks):
+            g = dist.new_group(list(ranks))
+            return DistComm(g) if dist.get_rank() in ranks else None
+    out = {}
+    for devs in sets:
+        comm = new_group(devs)
+        if comm is not None:
+            out[devs] = comm
+    return out
+
+
 def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, rank: int = 0, world: int = 1,
             model_name: str = "llama-3.1-8b", run_job: Callable | None = None,
-            steps_override: int | None = None, all_gather: Callable | None = None) -> dict:
+            steps_override: int | None = None, all_gather: Callable | None = None,
+            new_group: Callable | None = None) -> dict:
     """Execute this rank's share of the queue.  Returns a report with the per-job records
     (gathered from every rank when ``all_gather`` is given), profile records, the
     measured makespan (max over ranks of the per-device busy time) and the placement."""
     placement = place(queue, gpu_count)
-    for j in queue.jobs():
-        if j.degree != 1:
-            raise NotImplementedError(f"job {j.id} has degree {j.degree}: tensor-parallel jobs are not built yet")
+    groups = tp_groups(queue, placement, world, gpu_count, new_group)
     by_id = {c.id: c for c in configs}
     devices = list(range(rank, gpu_count, world))   # a rank drives every device = rank (mod world)
     records = []
@@ -106,11 +134,13 @@ def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, r
     for dev in devices:
         clock = 0.0
         for job in rank_schedule(queue, placement, dev):
+            comm = groups.get(placement.devices[job.id])
+            extra = {"tp": comm} if comm is not None else {}
             if run_job is None:
                 steps, dt, it, losses = train_packed_job(job, by_id, model_name, f"cuda:{dev % max(1, _ndev())}",
-                                                         steps_override)
+                                                         steps_override, **extra)
             else:
-                steps, dt, it, losses = run_job(job, by_id, dev)
+                steps, dt, it, losses = run_job(job, by_id, dev, **extra)
             records.append(JobRecord(job.id, dev, job.configs, steps, clock, dt, it, tuple(losses)))
             clock += dt
         t_dev[dev] = clock
@@ -119,8 +149,16 @@ def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, r
     all_records = [JobRecord(**{**r, "configs": tuple(r["configs"]), "losses": tuple(r["losses"])})
                    for g in gathered for r in g["records"]]
     busy = {int(k): v for g in gathered for k, v in g["busy_s"].items()}
-    profiles = [ProfileRecord(1, tuple(by_id[c].rank for c in r.configs), tuple(by_id[c].batch_size for c in r.configs),
-                              max(by_id[c].seq_len for c in r.configs), r.iter_time_s) for r in all_records]
+    # one profile record per job (a TP job reports from each of its ranks: keep the slowest)
+    degree = {j.id: j.degree for j in queue.jobs()}
+    per_job: dict = {}
+    for r in all_records:
+        if r.job_id not in per_job or r.iter_time_s > per_job[r.job_id].iter_time_s:
+            per_job[r.job_id] = r
+    profiles = [ProfileRecord(degree[r.job_id], tuple(by_id[c].rank for c in r.configs),
+                              tuple(by_id[c].batch_size for c in r.configs),
+                              max(by_id[c].seq_len for c in r.configs), r.iter_time_s)
+                for _, r in sorted(per_job.items())]
     return {"records": all_records, "profiles": profiles, "makespan_s": max(busy.values(), default=0.0),
             "busy_s": busy, "placement": placement}
 

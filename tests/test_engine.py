@@ -86,3 +86,52 @@ def test_profiles_calibrate_time_model():
     assert len(rep["profiles"]) == len(queue.jobs())
     tm = S.calibrate_time_model(rep["profiles"] * 1 + [S.ProfileRecord(1, (8,), (1,), 16, 0.11)])
     assert tm.has_degree(1)
+
+
+def _tp_instance(n=4, G=2):
+    """Adapters too big for one GPU at degree 1 but fitting at degree 2 -> degree-2 (TP) jobs."""
+    model = S.ModelSpec("m", 1, (S.TargetModule("q", 1 << 20, 1 << 20),), 0, 2)
+    configs = [S.LoraConfig(f"t{i:02d}", rank=8, alpha=16.0, batch_size=1, learning_rate=1e-4, seq_len=16,
+                            train_steps=2) for i in range(n)]
+    per = S.lora_state_memory(configs[0], model, S.ShardingSpec()).total_bytes
+    pool = S.GpuPool(G, int(per * 0.8))
+    tm = S.TimeModel(coeffs={1: (1.0, 1e-4), 2: (0.5, 0.5e-4)})
+    mem = S.MemoryContext(model, pool, configs)
+    return configs, S.plan_jobs(G, configs, tm, mem)
+
+
+def fake_run_tp(job, by_id, dev, tp=None):
+    import torch
+    assert tp is not None and tp.world == job.degree
+    x = torch.tensor([float(tp.rank + 1)])
+    tp.all_reduce_(x)                      # the job's own TP group
+    return 1, 0.5, 0.5, [float(x.item())]
+
+
+def _tp_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def gather(obj):
+        res = [None] * world
+        dist.all_gather_object(res, obj)
+        return res
+
+    configs, queue = _tp_instance()
+    rep = execute(queue, configs, world, rank=rank, world=world, run_job=fake_run_tp, all_gather=gather)
+    out[rank] = ([(r.job_id, r.device, r.losses) for r in rep["records"]], [p.parallelism_degree for p in rep["profiles"]])
+    dist.destroy_process_group()
+
+
+def test_engine_tensor_parallel_jobs_gloo():
+    configs, queue = _tp_instance()
+    assert queue.jobs() and all(j.degree == 2 for j in queue.jobs())
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_tp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    recs, degrees = out[0]
+    assert out[1][0] == recs
+    # every TP job ran on both devices, and its all-reduce summed 1 + 2 over the job's group
+    assert sorted((j, d) for j, d, _ in recs) == sorted((j.id, d) for j in queue.jobs() for d in (0, 1))
+    assert all(loss == (3.0,) for _, _, loss in recs)
+    assert degrees == [2] * len(queue.jobs())
