@@ -10,13 +10,16 @@ def classify(name: str) -> str:
     m = re.search(r"plora_gemm_pair_kernel<\(bool\)(\d), \(int\)(\d)>|plora_gemm_pair_kernel<(\w+), (\d)>", name)
     if "plora_gemm_pair_kernel" in name:
         return "gemm_pair (K1/K2b fwd, K6 dX, lm_head)"
+    if "plora_segred_lpt_kernel" in name:
+        return "segred (K3/K5)"
     if "plora_gemm_kernel" in name:
         if ", 1," in name or "(int)1," in name:
             return "shrink (K2a/K4)"
         if ", 2," in name or "(int)2," in name:
             return "segred (K3/K5)"
         return "gemm_1cta (N<256)"
-    for key in ("adamw", "rmsnorm_fwd", "rmsnorm_bwd", "swiglu_fwd", "swiglu_bwd", "rope", "ce_kernel"):
+    for key in ("adamw", "add_rmsnorm", "rmsnorm_fwd", "rmsnorm_bwd", "swiglu_fwd", "swiglu_bwd", "rope", "ce_kernel",
+                "ce_stats", "ce_apply"):
         if key in name:
             return key
     if "sdpa" in name or "fmha" in name or "cudnn" in name or "attention" in name:
