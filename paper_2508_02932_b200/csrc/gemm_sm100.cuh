@@ -510,6 +510,49 @@ __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx)
 
 __device__ __forceinline__ uint32_t peer_masked(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
 
+// Pair-kernel epilogue: one 32 x 32 bf16 chunk out of registers -- staged through the
+// warp's two 2 KB smem buffers (64-byte swizzle) into a TMA store / reduce-add for full
+// 32-row warps, masked direct stores otherwise.
+__device__ __forceinline__ void pair_emit_chunk(const GemmArgs& args, uint8_t* stg, int& issued, int lane, int col0,
+                                                int m0, int m_len, const uint32_t (&v)[16]) {
+  if (col0 >= args.N) return;
+  if (m_len == 32) {
+    uint8_t* buf = stg + (issued & 1) * 2048;
+    if (issued >= 2) {
+      if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has read it
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(buf + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) =
+          make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (args.accumulate) tma_reduce_add_2d(&args.tmY, buf, col0, m0);
+      else                 tma_store_2d(&args.tmY, buf, col0, m0);
+      bulk_commit();
+    }
+    ++issued;
+  } else if (lane < m_len) {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(m0 + lane) * args.ldo;
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int cc = col0 + 2 * q;
+      if (cc < args.N) {
+        float2 f = __bfloat1622float2(h[q]);
+        if (args.accumulate) {
+          const float2 old = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + cc));
+          f.x += old.x;
+          f.y += old.y;
+        }
+        *reinterpret_cast<__nv_bfloat162*>(o + cc) = __floats2bfloat162_rn(f.x, f.y);
+      }
+    }
+  }
+}
+
 template <bool B_MN, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
     plora_gemm_pair_kernel(const __grid_constant__ GemmArgs args) {
@@ -677,46 +720,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       const int c0 = chalf * kChunks;
       const bool skip = (args.debug & 1) != 0;
       const bool store = !skip && !(args.debug & 4) && m_len > 0;   // bit 2: TMEM drain only (experiment)
-      // one chunk out of registers: staged TMA store for full 32-row warps, masked stores otherwise
-      auto emit = [&](int j, const uint32_t (&v)[16]) {
-        const int col0 = t.n0 + (c0 + j) * 32;
-        if (col0 >= args.N) return;
-        if (m_len == 32) {
-          uint8_t* buf = stg + (issued & 1) * 2048;
-          if (issued >= 2) {
-            if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has read it
-            __syncwarp();
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(buf + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) =
-                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (args.accumulate) tma_reduce_add_2d(&args.tmY, buf, col0, m0);
-            else                 tma_store_2d(&args.tmY, buf, col0, m0);
-            bulk_commit();
-          }
-          ++issued;
-        } else if (lane < m_len) {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(m0 + lane) * args.ldo;
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int cc = col0 + 2 * q;
-            if (cc < args.N) {
-              float2 f = __bfloat1622float2(h[q]);
-              if (args.accumulate) {
-                const float2 old = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + cc));
-                f.x += old.x;
-                f.y += old.y;
-              }
-              *reinterpret_cast<__nv_bfloat162*>(o + cc) = __floats2bfloat162_rn(f.x, f.y);
-            }
-          }
-        }
-      };
       uint32_t pk[kParked > 0 ? kParked : 1][16];
       if (!skip) {
         uint32_t r[32];
@@ -729,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
             if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c0 + j + 1) * 32, r);   // overlaps the store below
-            if (store) emit(j, v);
+            if (store) pair_emit_chunk(args, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, v);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
@@ -744,7 +747,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       if (++acc == AS) { acc = 0; acc_phase ^= 1; }
       if (!store) continue;
 #pragma unroll
-      for (int j = kDirect; j < kChunks; ++j) emit(j, pk[j - kDirect]);
+      for (int j = kDirect; j < kChunks; ++j)
+        pair_emit_chunk(args, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, pk[j - kDirect]);
     }
     if (lane == 0) bulk_wait<0>();   // all TMA stores complete before the CTA retires
     __syncwarp();

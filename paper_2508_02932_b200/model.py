@@ -200,6 +200,8 @@ class _LayerSave:
     g: torch.Tensor
     u: torch.Tensor
     hs: dict = field(default_factory=dict)
+    x1: torch.Tensor | None = None     # normed inputs, kept when memory allows (else recomputed)
+    x2: torch.Tensor | None = None
 
 
 class PackedLoraTrainer:
@@ -207,7 +209,8 @@ class PackedLoraTrainer:
 
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
-                 a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None):
+                 a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
+                 save_normed: bool | None = None):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the all-reduces described in tp.py."""
@@ -245,9 +248,27 @@ class PackedLoraTrainer:
         self.has_label = pos != seq_len - 1
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
+        self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
+    def activation_bytes(self, save_normed: bool) -> int:
+        """Saved-activation estimate of one step (bf16): per layer h_in, h_mid, q/k/v, the
+        attention output, gate/up and the 7 Hs tiles (+ the two normed inputs)."""
+        cfg, T, hd = self.cfg, self.T, self.cfg.head_dim
+        ffn_l = self.targets[4].h_out
+        per = (2 * cfg.d + (self.H_l + 2 * self.KV_l) * hd + self.H_l * hd + 2 * ffn_l
+               + 7 * self.meta.rpad64 + (2 * cfg.d if save_normed else 0))
+        return 2 * T * per * cfg.n_layers
+
+    def _fits_saved_norms(self) -> bool:
+        """Keep x1/x2 from the forward (saves two RMSNorm recomputes per layer) when the
+        extra activations leave >= 12 GB of headroom on the device."""
+        if self.device.type != "cuda":
+            return False
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return free - self.activation_bytes(True) > 12e9
+
     def _lin_fwd(self, layer: int, tname: str, x: torch.Tensor, w: torch.Tensor, residual=None):
         a_sh = self.bank.shadow_of(layer, tname, "A")
         bt_sh = self.bank.shadow_of(layer, tname, "B")
@@ -321,6 +342,7 @@ class PackedLoraTrainer:
         else:
             h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
         (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1)
+        x1_keep = x1 if self.save_normed else None
         del x1
         if cfg.qkv_bias:
             q += lw["q_bias"]
@@ -339,13 +361,15 @@ class PackedLoraTrainer:
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
         (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2)
+        x2_keep = x2 if self.save_normed else None
         del x2
         act = ew.swiglu_fwd(g, u)
         d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
         self._reduce(d_out, hs_d)
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
                           attn_out=attn, g=g, u=u,
-                          hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d})
+                          hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d},
+                          x1=x1_keep, x2=x2_keep)
         return h_mid, d_out, save
 
     # ------------------------------------------------------------------ backward
@@ -366,7 +390,8 @@ class PackedLoraTrainer:
         del d_act
         ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
         del act, dh_down
-        x2 = ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
+        x2 = sv.x2 if sv.x2 is not None else ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
+        sv.x2 = None
         dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))
         self._reduce(dx2)
         del dg, du, x2
@@ -379,7 +404,8 @@ class PackedLoraTrainer:
         dq = ew.rope(dq.transpose(1, 2), self.cos, self.sin, s, inverse=True)      # [T][H*hd]
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
         dv = self._token_major(dv)
-        x1 = ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
+        x1 = sv.x1 if sv.x1 is not None else ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
+        sv.x1 = None
         dx1 = self._group_bwd(layer, ("v", "k", "q"), x1, (sv.hs["v"], sv.hs["k"], sv.hs["q"]), (dv, dk, dq),
                               need_dx=need_dx)
         del dq, dk, dv, x1

@@ -109,3 +109,18 @@ def test_packing_invariance_model_level():
             a = packed.bank.block(packed.bank.G, layer, t, "A", i)
             b = solo.bank.block(solo.bank.G, layer, t, "A", 0)
             assert O.rel_frobenius(b.cpu().numpy(), a.cpu().numpy()) <= 1e-2
+
+
+def test_saved_and_recomputed_norms_bit_identical():
+    """Keeping the normed inputs x1/x2 from the forward (save_normed) and recomputing
+    them from (h, rstd) in the backward give bit-identical losses and gradients."""
+    cfg = PRESETS["tiny"]
+    sp, s = bench_adapters("tiny")
+    kw = dict(device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in sp])
+    a = PackedLoraTrainer(cfg, sp, s, save_normed=True, **kw)
+    b = PackedLoraTrainer(cfg, sp, s, save_normed=False, base=a.base, **kw)
+    tokens = a.synthetic_tokens().cuda()
+    la = a.forward_backward(tokens).clone()
+    lb = b.forward_backward(tokens).clone()
+    assert torch.equal(la, lb)
+    assert torch.equal(a.bank.G, b.bank.G)
