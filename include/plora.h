@@ -143,6 +143,22 @@ PLORA_API int plora_linear_expand(void* stream, const plora_pack_t* pack,
                      const void* W, int32_t w_kmajor, const void* Bt_sh,
                      const void* Hs, void* Y, int64_t ldy, const void* residual);
 
+/* Grouped K1 + K2b for n (1..3) targets sharing the input X (q/k/v, gate/up): ONE
+ * launch enumerates every target's output tiles (N-segments of the pair GEMM);
+ * Y[j] bf16 [T][k_out[j]] = X op(W[j]) + Hs[j]_i Bt_sh[j]_i^T.  W / Bt_sh / Hs / Y are
+ * host arrays of n device pointers. */
+PLORA_API int plora_linear_expand_group(void* stream, const plora_pack_t* pack,
+                     const void* X, int64_t d, int32_t n, const int64_t* k_out,
+                     const void* const* W, int32_t w_kmajor, const void* const* Bt_sh,
+                     const void* const* Hs, void* const* Y);
+
+/* Grouped K6 for those targets: dX [T][lddx] = sum_j dY[j] op(W[j])^T + dH[j]_i A_sh[j]_i^T
+ * (+ dX_residual), one accumulator over the concatenated K range (K-segments). */
+PLORA_API int plora_linear_dx_group(void* stream, const plora_pack_t* pack, int32_t n,
+                     const void* const* dY, const int64_t* k_out, const void* const* W,
+                     int32_t w_kmajor, const void* const* A_sh, const void* const* dH,
+                     int64_t d, void* dX, int64_t lddx, const void* dX_residual);
+
 /* Packed LoRA linear, backward (reference packed_backward, lorapack.py:202-231):
  *   dH  = alpha_i dY_i B_i^T                       (Case 2, K4 shrink)
  *   dB_i^T = Hs_i^T dY_i  -> gradB (f32)           (Case 1, K3 segment reduction)

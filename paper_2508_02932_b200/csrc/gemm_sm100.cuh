@@ -472,12 +472,42 @@ struct PairCfg {
   static constexpr int kBand = 8;                           // pair tiles per raster band
 };
 
+// Segmented pair GEMM: up to 3 problems sharing one accumulator schedule.
+//  * N-segments (n_seg > 1, k_seg == 1): targets that share the input X (q/k/v, gate/up)
+//    -- one launch, the output tiles of every target enumerated together; target s has
+//    its own weight, LoRA operands and output.
+//  * K-segments (k_seg > 1, n_seg == 1): input gradients of those targets, which sum
+//    into ONE dX = sum_s dY_s W_s + dH_s A_s^T -- one accumulator over the concatenated
+//    K range (fp32 in TMEM, no bf16 read-modify-write between targets).
+// Segment 0 uses g.tmA/tmB/tmH/tmL/tmY; segments 1, 2 the arrays below.
+struct __align__(64) PairArgs {
+  GemmArgs g;
+  CUtensorMap tmA2[2];
+  CUtensorMap tmB2[2];
+  CUtensorMap tmH2[2];
+  CUtensorMap tmL2[2];
+  CUtensorMap tmY2[2];
+  int32_t n_seg;
+  int32_t k_seg;
+  int32_t seg_nt_end[3];   // N-segments: cumulative n-tile counts
+  int32_t seg_N[3];        // N-segments: valid output columns
+  int32_t seg_kb_end[3];   // K-segments: cumulative main K-block counts
+  int32_t pad_;
+  void* seg_out[3];        // N-segments: output base (masked direct stores)
+  int64_t seg_ldo[3];
+};
+
+__device__ __forceinline__ const CUtensorMap* seg_map(const CUtensorMap* m0, const CUtensorMap* rest, int s) {
+  return s == 0 ? m0 : rest + (s - 1);
+}
+
 struct PairTile {
-  int m0, m_len, adapter, n0, n_main, n_lora, rank;
+  int m0, m_len, adapter, n0, n_main, n_lora, rank, seg, nlps;
 };
 
 template <int NB>
-__device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx) {
+__device__ __forceinline__ PairTile decode_pair_tile(const PairArgs& p, int idx) {
+  const GemmArgs& a = p.g;
   PairTile t;
   const int per_band = PairCfg<NB>::kBand * a.n_ntiles;
   const int band = idx / per_band;
@@ -496,13 +526,18 @@ __device__ __forceinline__ PairTile decode_pair_tile(const GemmArgs& a, int idx)
     t.m_len = min(256, a.M - t.m0);
     t.adapter = 0;
   }
-  t.n0 = nt * PairCfg<NB>::kBN;
-  t.n_main = (a.K + kBK - 1) / kBK;
+  int sg = 0;
+  while (sg + 1 < p.n_seg && nt >= p.seg_nt_end[sg]) ++sg;
+  t.seg = sg;
+  t.n0 = (nt - (sg ? p.seg_nt_end[sg - 1] : 0)) * PairCfg<NB>::kBN;
+  t.n_main = p.seg_kb_end[p.k_seg - 1];
   if (a.has_lora) {
     t.rank = a.ranks[t.adapter];
-    t.n_lora = min((t.rank + 63) / 64, a.nb);
+    t.nlps = min((t.rank + 63) / 64, a.nb);
+    t.n_lora = t.nlps * p.k_seg;
   } else {
     t.rank = 0;
+    t.nlps = 0;
     t.n_lora = 0;
   }
   return t;
@@ -513,9 +548,17 @@ __device__ __forceinline__ uint32_t peer_masked(const void* p) { return smem_u32
 // Pair-kernel epilogue: one 32 x 32 bf16 chunk out of registers -- staged through the
 // warp's two 2 KB smem buffers (64-byte swizzle) into a TMA store / reduce-add for full
 // 32-row warps, masked direct stores otherwise.
-__device__ __forceinline__ void pair_emit_chunk(const GemmArgs& args, uint8_t* stg, int& issued, int lane, int col0,
+struct PairOut {
+  const CUtensorMap* tm;
+  __nv_bfloat16* out;
+  int64_t ldo;
+  int N;
+  int accumulate;
+};
+
+__device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg, int& issued, int lane, int col0,
                                                 int m0, int m_len, const uint32_t (&v)[16]) {
-  if (col0 >= args.N) return;
+  if (col0 >= po.N) return;
   if (m_len == 32) {
     uint8_t* buf = stg + (issued & 1) * 2048;
     if (issued >= 2) {
@@ -529,20 +572,20 @@ __device__ __forceinline__ void pair_emit_chunk(const GemmArgs& args, uint8_t* s
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      if (args.accumulate) tma_reduce_add_2d(&args.tmY, buf, col0, m0);
-      else                 tma_store_2d(&args.tmY, buf, col0, m0);
+      if (po.accumulate) tma_reduce_add_2d(po.tm, buf, col0, m0);
+      else               tma_store_2d(po.tm, buf, col0, m0);
       bulk_commit();
     }
     ++issued;
   } else if (lane < m_len) {
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(m0 + lane) * args.ldo;
+    __nv_bfloat16* o = po.out + static_cast<int64_t>(m0 + lane) * po.ldo;
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int cc = col0 + 2 * q;
-      if (cc < args.N) {
+      if (cc < po.N) {
         float2 f = __bfloat1622float2(h[q]);
-        if (args.accumulate) {
+        if (po.accumulate) {
           const float2 old = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + cc));
           f.x += old.x;
           f.y += old.y;
@@ -555,8 +598,9 @@ __device__ __forceinline__ void pair_emit_chunk(const GemmArgs& args, uint8_t* s
 
 template <bool B_MN, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
-    plora_gemm_pair_kernel(const __grid_constant__ GemmArgs args) {
+    plora_gemm_pair_kernel(const __grid_constant__ PairArgs p) {
   using Cfg = PairCfg<NB>;
+  const GemmArgs& args = p.g;
   constexpr int S = Cfg::kStages;
   constexpr int AS = Cfg::kAccStages;
   extern __shared__ uint8_t smem_raw[];
@@ -575,12 +619,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
   const int n_clusters = gridDim.x >> 1;
   const int total = args.n_groups * args.n_ntiles;
 
+  const int nseg = p.n_seg > p.k_seg ? p.n_seg : p.k_seg;
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&args.tmA);
-    tma_prefetch(&args.tmB);
-    if (args.has_lora) {
-      tma_prefetch(&args.tmH);
-      tma_prefetch(&args.tmL);
+    for (int sg = 0; sg < nseg; ++sg) {
+      if (sg == 0 || p.k_seg > 1) tma_prefetch(seg_map(&args.tmA, p.tmA2, sg));
+      tma_prefetch(seg_map(&args.tmB, p.tmB2, sg));
+      if (args.has_lora) {
+        tma_prefetch(seg_map(&args.tmH, p.tmH2, sg));
+        tma_prefetch(seg_map(&args.tmL, p.tmL2, sg));
+      }
     }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);   // leader: one arrive.expect_tx per phase (both CTAs' bytes)
@@ -605,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       uint32_t phase = 0;
       const int half = static_cast<int>(rank) * 128;
       for (int idx = cluster; idx < total; idx += n_clusters) {
-        const PairTile t = decode_pair_tile<NB>(args, idx);
+        const PairTile t = decode_pair_tile<NB>(p, idx);
         const int nblk = t.n_main + t.n_lora;
         for (int b = 0; b < nblk; ++b) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -619,24 +666,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
           if (leader) mbar_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
           const uint32_t fb = peer_masked(&full_bar[stage]);
           if (b < t.n_main) {
-            const int kc = b * kBK;
-            tma_load_2d_pair(sA, &args.tmA, fb, kc, t.m0 + half);
+            int ks = 0;   // K-segment of this K-block
+            while (ks + 1 < p.k_seg && b >= p.seg_kb_end[ks]) ++ks;
+            const int kc = (b - (ks ? p.seg_kb_end[ks - 1] : 0)) * kBK;
+            const CUtensorMap* mA = seg_map(&args.tmA, p.tmA2, ks);
+            const CUtensorMap* mB = seg_map(&args.tmB, p.tmB2, p.k_seg > 1 ? ks : t.seg);
+            tma_load_2d_pair(sA, mA, fb, kc, t.m0 + half);
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
               const int n = t.n0 + 256 * c + half;
               if (B_MN) {
-                tma_load_2d_pair(sB + c * 16384, &args.tmB, fb, n, kc);
-                tma_load_2d_pair(sB + c * 16384 + 8192, &args.tmB, fb, n + 64, kc);
+                tma_load_2d_pair(sB + c * 16384, mB, fb, n, kc);
+                tma_load_2d_pair(sB + c * 16384 + 8192, mB, fb, n + 64, kc);
               } else {
-                tma_load_2d_pair(sB + c * 16384, &args.tmB, fb, kc, n);
+                tma_load_2d_pair(sB + c * 16384, mB, fb, kc, n);
               }
             }
           } else {
             const int lb = b - t.n_main;
-            tma_load_2d_pair(sA, &args.tmH, fb, lb * 64, t.m0 + half);
+            const int ls = p.k_seg > 1 ? lb / t.nlps : t.seg;   // LoRA operands of this segment
+            const int lbs = p.k_seg > 1 ? lb - ls * t.nlps : lb;
+            tma_load_2d_pair(sA, seg_map(&args.tmH, p.tmH2, ls), fb, lbs * 64, t.m0 + half);
 #pragma unroll
             for (int c = 0; c < NB; ++c)
-              tma_load_3d_pair(sB + c * 16384, &args.tmL, fb, lb * 64, t.n0 + 256 * c + half, t.adapter);
+              tma_load_3d_pair(sB + c * 16384, seg_map(&args.tmL, p.tmL2, ls), fb, lbs * 64, t.n0 + 256 * c + half,
+                               t.adapter);
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -652,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int idx = cluster; idx < total; idx += n_clusters) {
-        const PairTile t = decode_pair_tile<NB>(args, idx);
+        const PairTile t = decode_pair_tile<NB>(p, idx);
         const int nblk = t.n_main + t.n_lora;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -666,7 +720,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
             const uint32_t a0 = smem_u32(sA);
             const uint32_t b0 = smem_u32(sB);
             const bool lora = b >= t.n_main;
-            const int ksteps = lora ? min(4, (t.rank - (b - t.n_main) * 64 + 15) / 16) : 4;
+            const int lbs = lora ? (p.k_seg > 1 ? (b - t.n_main) % t.nlps : b - t.n_main) : 0;
+            const int ksteps = lora ? min(4, (t.rank - lbs * 64 + 15) / 16) : 4;
             for (int ks = 0; ks < ksteps; ++ks) {
               const uint64_t ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
 #pragma unroll
@@ -711,7 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     uint32_t acc_phase = 0;
     int issued = 0;
     for (int idx = cluster; idx < total; idx += n_clusters) {
-      const PairTile t = decode_pair_tile<NB>(args, idx);
+      const PairTile t = decode_pair_tile<NB>(p, idx);
       const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;   // this warp's 32 rows
       const int m_len = min(32, t.m_len - static_cast<int>(rank) * 128 - quarter * 32);
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -720,6 +775,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       const int c0 = chalf * kChunks;
       const bool skip = (args.debug & 1) != 0;
       const bool store = !skip && !(args.debug & 4) && m_len > 0;   // bit 2: TMEM drain only (experiment)
+      PairOut po;
+      po.tm = seg_map(&args.tmY, p.tmY2, t.seg);
+      po.out = static_cast<__nv_bfloat16*>(p.seg_out[t.seg]);
+      po.ldo = p.seg_ldo[t.seg];
+      po.N = p.seg_N[t.seg];
+      po.accumulate = args.accumulate;
       uint32_t pk[kParked > 0 ? kParked : 1][16];
       if (!skip) {
         uint32_t r[32];
@@ -732,7 +793,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
             if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c0 + j + 1) * 32, r);   // overlaps the store below
-            if (store) pair_emit_chunk(args, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, v);
+            if (store) pair_emit_chunk(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, v);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
@@ -748,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       if (!store) continue;
 #pragma unroll
       for (int j = kDirect; j < kChunks; ++j)
-        pair_emit_chunk(args, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, pk[j - kDirect]);
+        pair_emit_chunk(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, pk[j - kDirect]);
     }
     if (lane == 0) bulk_wait<0>();   // all TMA stores complete before the CTA retires
     __syncwarp();

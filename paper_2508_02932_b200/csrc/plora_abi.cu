@@ -165,14 +165,14 @@ static bool g_pair_enabled = [] {
 }();
 
 template <bool B_MN, int NB>
-static int launch_pair(const GemmArgs& args, cudaStream_t stream) {
+static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   auto kern = plora_gemm_pair_kernel<B_MN, NB>;
   static bool configured = false;
   if (!configured) {
     PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<NB>::kSmemBytes));
     configured = true;
   }
-  const int total = args.n_groups * args.n_ntiles;
+  const int total = args.g.n_groups * args.g.n_ntiles;
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
   const int clusters = total < max_clusters ? total : max_clusters;
@@ -186,23 +186,75 @@ static int g_pair_nb_min_n = [] {   // N at which the 256x512 pair tile is used
   return e ? atoi(e) : 2048;
 }();
 
-// CTA-pair GEMM (N >= 256): 256 x 256 tiles with tcgen05 cta_group::2.
-static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
-                         const void* A, const void* W, int w_kmajor, const void* H, const void* L,
-                         void* Y, int64_t ldy, const void* residual) {
-  const int NB = N >= g_pair_nb_min_n ? 2 : 1;
-  GemmArgs a;
-  memset(&a, 0, sizeof(a));
-  int rc = make_map_2d(&a.tmA, A, K, M, K, 64, kBM);
-  if (rc) return rc;
-  if (w_kmajor) rc = make_map_2d(&a.tmB, W, K, N, K, 64, 128);
-  else          rc = make_map_2d(&a.tmB, W, N, K, N, 64, 64);
-  if (rc) return rc;
-  const bool lora = pack != nullptr && H != nullptr && L != nullptr;
+// One segment of a (segmented) pair GEMM; see PairArgs in gemm_sm100.cuh.
+struct PairSeg {
+  const void* A;   // [M][K] (K-segments: per segment; N-segments: segment 0's is shared)
+  int64_t K;
+  const void* W;   // w_kmajor ? [N][K] : [K][N]
+  int64_t N;
+  const void* H;   // LoRA A operand [M][64nb] (may be NULL: no LoRA)
+  const void* L;   // LoRA B operand [n][N][64nb]
+  void* Y;         // [M][ldy] (K-segments: segment 0's is the shared output)
+  int64_t ldy;
+};
+
+// CTA-pair GEMM over 1..3 N-segments (shared A) or K-segments (shared output).
+static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t M, int n_seg, int k_seg,
+                             const PairSeg* sg, int w_kmajor, const void* residual) {
+  if (n_seg < 1 || k_seg < 1 || n_seg > 3 || k_seg > 3 || (n_seg > 1 && k_seg > 1))
+    return fail("pair gemm: 1..3 N-segments or 1..3 K-segments");
+  const int nseg = n_seg > k_seg ? n_seg : k_seg;
+  int64_t Nmin = sg[0].N;
+  for (int s = 1; s < n_seg; ++s) Nmin = sg[s].N < Nmin ? sg[s].N : Nmin;
+  int64_t Ntot = 0;
+  for (int s = 0; s < n_seg; ++s) Ntot += sg[s].N;
+  const int NB = (n_seg > 1 ? Ntot : Nmin) >= g_pair_nb_min_n ? 2 : 1;
+  const int tile_n = 256 * NB;
+  PairArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  GemmArgs& a = pa.g;
+  CUtensorMap* mA[3] = {&a.tmA, &pa.tmA2[0], &pa.tmA2[1]};
+  CUtensorMap* mB[3] = {&a.tmB, &pa.tmB2[0], &pa.tmB2[1]};
+  CUtensorMap* mH[3] = {&a.tmH, &pa.tmH2[0], &pa.tmH2[1]};
+  CUtensorMap* mL[3] = {&a.tmL, &pa.tmL2[0], &pa.tmL2[1]};
+  CUtensorMap* mY[3] = {&a.tmY, &pa.tmY2[0], &pa.tmY2[1]};
+  const bool lora = pack != nullptr && sg[0].H != nullptr && sg[0].L != nullptr;
+  const int64_t R64 = pack ? 64LL * pack->nb : 64;
+  int rc;
+  int nt = 0, kb = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const PairSeg& g = sg[s];
+    const int64_t K = (k_seg > 1) ? g.K : sg[0].K;
+    const int64_t N = (n_seg > 1) ? g.N : sg[0].N;
+    if (K <= 0 || K % 8 || N % 8) return fail("pair gemm: K and N must be positive multiples of 8");
+    if (s == 0 || k_seg > 1)
+      if ((rc = make_map_2d(mA[s], g.A, K, M, K, 64, kBM))) return rc;
+    if (w_kmajor) rc = make_map_2d(mB[s], g.W, K, N, K, 64, 128);
+    else          rc = make_map_2d(mB[s], g.W, N, K, N, 64, 64);
+    if (rc) return rc;
+    if (lora) {
+      if (!g.H || !g.L) return fail("pair gemm: every segment needs its LoRA operands");
+      if ((rc = make_map_2d(mH[s], g.H, R64, M, R64, 64, kBM))) return rc;
+      if ((rc = make_map_3d(mL[s], g.L, R64, N, pack->n_adapters, 64, 128))) return rc;
+    }
+    if (s == 0 || n_seg > 1) {
+      if (!g.Y || g.ldy % 8 || reinterpret_cast<uintptr_t>(g.Y) % 16)
+        return fail("pair gemm: output must be 16-byte aligned with ldy a multiple of 8");
+      if ((rc = make_map_out(mY[s], g.Y, N, M, g.ldy))) return rc;
+      pa.seg_out[s] = g.Y;
+      pa.seg_ldo[s] = g.ldy;
+      pa.seg_N[s] = static_cast<int>(N);
+      nt += static_cast<int>((N + tile_n - 1) / tile_n);
+      pa.seg_nt_end[s] = nt;
+    }
+    if (s == 0 || k_seg > 1) {
+      kb += static_cast<int>((K + kBK - 1) / kBK);
+      pa.seg_kb_end[s] = kb;
+    }
+  }
+  pa.n_seg = n_seg;
+  pa.k_seg = k_seg;
   if (lora) {
-    const int64_t R64 = 64LL * pack->nb;
-    if ((rc = make_map_2d(&a.tmH, H, R64, M, R64, 64, kBM))) return rc;
-    if ((rc = make_map_3d(&a.tmL, L, R64, N, pack->n_adapters, 64, 128))) return rc;
     a.ranks = pack->d_ranks;
     a.nb = pack->nb;
     a.has_lora = 1;
@@ -210,22 +262,27 @@ static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, i
   a.mtiles = pack ? pack->d_ptiles : nullptr;
   a.n_groups = pack ? pack->n_ptiles : static_cast<int>((M + 255) / 256);
   a.M = static_cast<int>(M);
-  a.N = static_cast<int>(N);
-  a.K = static_cast<int>(K);
-  a.n_ntiles = static_cast<int>((N + 256 * NB - 1) / (256 * NB));
-  a.out = Y;
-  a.ldo = ldy;
-  if ((rc = make_map_out(&a.tmY, Y, N, M, ldy))) return rc;
+  a.n_ntiles = nt;
   // Y = result + residual is computed as Y <- residual (skipped when in place), then a
   // TMA reduce-add of the result (bf16 add in L2).
   if (residual) {
-    if (residual != Y)
-      PLORA_CUDA(cudaMemcpy2DAsync(Y, ldy * 2, residual, ldy * 2, N * 2, M, cudaMemcpyDeviceToDevice, st));
+    if (n_seg > 1) return fail("pair gemm: residual needs a single output");
+    if (residual != sg[0].Y)
+      PLORA_CUDA(cudaMemcpy2DAsync(sg[0].Y, sg[0].ldy * 2, residual, sg[0].ldy * 2, sg[0].N * 2, M,
+                                   cudaMemcpyDeviceToDevice, st));
     a.accumulate = 1;
   }
   a.debug = g_debug_flags;
-  if (NB == 2) return w_kmajor ? launch_pair<false, 2>(a, st) : launch_pair<true, 2>(a, st);
-  return w_kmajor ? launch_pair<false, 1>(a, st) : launch_pair<true, 1>(a, st);
+  if (NB == 2) return w_kmajor ? launch_pair<false, 2>(pa, st) : launch_pair<true, 2>(pa, st);
+  return w_kmajor ? launch_pair<false, 1>(pa, st) : launch_pair<true, 1>(pa, st);
+}
+
+// CTA-pair GEMM (N >= 256), one problem.
+static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
+                         const void* A, const void* W, int w_kmajor, const void* H, const void* L,
+                         void* Y, int64_t ldy, const void* residual) {
+  PairSeg sg{A, K, W, N, H, L, Y, ldy};
+  return run_pair_segments(st, pack, M, 1, 1, &sg, w_kmajor, residual);
 }
 
 // Base GEMM (+ fused LoRA expand).  A: [M][K] K-major.  W: see w_kmajor.
@@ -560,6 +617,56 @@ int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, i
   if ((rc = check_pack(pack))) return rc;
   return run_gemm(static_cast<cudaStream_t>(stream), pack, pack->total_tokens, k, d, X, W, w_kmajor,
                   Hs, Bt_sh, Y, ldy, residual);
+}
+
+static bool group_pair_ok(const plora_pack_t* pack, int n, const int64_t* N) {
+  if (!g_pair_enabled || (pack->d_ptiles == nullptr && pack->n_ptiles != 0)) return false;
+  for (int j = 0; j < n; ++j)
+    if (N[j] < 256) return false;
+  return true;
+}
+
+int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int32_t n,
+                              const int64_t* k_out, const void* const* W, int32_t w_kmajor,
+                              const void* const* Bt_sh, const void* const* Hs, void* const* Y) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (n < 1 || n > 3) return fail("expand_group: 1..3 targets");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t T = pack->total_tokens;
+  if (T <= 0) return 0;
+  if (!group_pair_ok(pack, n, k_out)) {   // narrow targets: one launch per target
+    for (int j = 0; j < n; ++j)
+      if ((rc = run_gemm(st, pack, T, k_out[j], d, X, W[j], w_kmajor, Hs[j], Bt_sh[j], Y[j], k_out[j], nullptr)))
+        return rc;
+    return 0;
+  }
+  PairSeg sg[3];
+  for (int j = 0; j < n; ++j) sg[j] = PairSeg{X, d, W[j], k_out[j], Hs[j], Bt_sh[j], Y[j], k_out[j]};
+  return run_pair_segments(st, pack, T, n, 1, sg, w_kmajor, nullptr);
+}
+
+int plora_linear_dx_group(void* stream, const plora_pack_t* pack, int32_t n, const void* const* dY,
+                          const int64_t* k_out, const void* const* W, int32_t w_kmajor, const void* const* A_sh,
+                          const void* const* dH, int64_t d, void* dX, int64_t lddx, const void* dX_residual) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (n < 1 || n > 3) return fail("dx_group: 1..3 targets");
+  if (!dX) return fail("dx_group: dX is NULL");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t T = pack->total_tokens;
+  if (T <= 0) return 0;
+  const int64_t dd[3] = {d, d, d};
+  if (!group_pair_ok(pack, 1, dd)) {
+    for (int j = 0; j < n; ++j)
+      if ((rc = run_gemm(st, pack, T, d, k_out[j], dY[j], W[j], !w_kmajor, dH[j], A_sh[j], dX, lddx,
+                         j == 0 ? dX_residual : dX)))
+        return rc;
+    return 0;
+  }
+  PairSeg sg[3];
+  for (int j = 0; j < n; ++j) sg[j] = PairSeg{dY[j], k_out[j], W[j], d, dH[j], A_sh[j], dX, lddx};
+  return run_pair_segments(st, pack, T, 1, n, sg, !w_kmajor, dX_residual);
 }
 
 int plora_linear_bwd(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int64_t k,

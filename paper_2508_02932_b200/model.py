@@ -285,30 +285,30 @@ class PackedLoraTrainer:
 
     def _group_fwd(self, layer: int, names, x: torch.Tensor):
         """Forward of targets sharing the input x (q/k/v or gate/up): ONE K2a launch reads
-        x once for every target's Hs, then per target the K1 GEMM with K2b fused."""
+        x once for every target's Hs, then ONE grouped K1 GEMM (K2b fused) for all targets."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
         hss = [torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device) for _ in names]
         ops.shrink_multi(meta, x, [bank.shadow_of(layer, nm, "A") for nm in names], hss)
-        ys = [ops.linear_expand(meta, x, lw[nm], True, bank.shadow_of(layer, nm, "B"), hs)
-              for nm, hs in zip(names, hss)]
+        ys = ops.linear_expand_group(meta, x, [lw[nm] for nm in names],
+                                     [bank.shadow_of(layer, nm, "B") for nm in names], hss)
         return ys, hss
 
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
-        """Backward of targets sharing the input x: per target K4 dH, K3 dB and the K6 dX
-        GEMM accumulated into one input gradient; then ONE K5 launch for every dA
-        (x read once).  Column-parallel under TP: dH_s and dX_s are partial, dH is
+        """Backward of targets sharing the input x: per target K4 dH and K3 dB; ONE grouped
+        K6 launch sums every target's input gradient in one fp32 accumulator; ONE K5
+        launch for every dA (x read once).  Column-parallel under TP: dH_s and dX_s are partial, dH is
         all-reduced before dA (tp.py), dX by the caller."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
-        dx = None
         dhs = []
         for nm, hs, dy in zip(names, hss, dys):
             dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
             ops.shrink(meta, dy, bank.shadow_of(layer, nm, "B"), dh)                        # K4 (Case 2)
             ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, nm, "B"))              # K3 (Case 1)
-            if need_dx:                                                                     # K6 (Case 4)
-                dx = ops.linear_expand(meta, dy, lw[nm], False, bank.shadow_of(layer, nm, "A"), dh,
-                                       y_out=dx, residual=dx)
             dhs.append(dh)
+        dx = None
+        if need_dx:   # K6 (Case 4) for every target in one accumulator
+            dx = ops.linear_dx_group(meta, list(dys), [lw[nm] for nm in names],
+                                     [bank.shadow_of(layer, nm, "A") for nm in names], dhs, x.shape[1])
         self._reduce(*dhs)
         ops.segred_multi(meta, x, dhs, [bank.region_flat(bank.G, layer, nm, "A") for nm in names])  # K5
         return dx

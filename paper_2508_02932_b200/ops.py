@@ -198,6 +198,54 @@ def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
     return gs
 
 
+def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmajor: bool = True) -> list:
+    """K1 + K2b for targets sharing x (q/k/v, gate/up) in ONE pair-GEMM launch:
+    y_j = x op(W_j) + Hs_j,i B_j,i (returns the new y_j [T][k_j])."""
+    T, d = x.shape
+    ks = [w.shape[0] if w_kmajor else w.shape[1] for w in ws]
+    ys = [torch.empty((T, k), dtype=torch.bfloat16, device=x.device) for k in ks]
+    karr = (ctypes.c_int64 * len(ks))(*ks)
+    t = _TIMER.start() if _TIMER else None
+    wp, _k1 = _ptr_array(ws, "w")
+    bp, _k2 = _ptr_array(bt_shs, "bt_sh")
+    hp, _k3 = _ptr_array(hss, "hs")
+    yp, _k4 = _ptr_array(ys, "y")
+    _lib.check(_lib.lib().plora_linear_expand_group(_stream(), ctypes.byref(meta.struct), _need(x, "x"), d, len(ws),
+                                                    karr, wp, int(w_kmajor), bp, hp, yp), "plora_linear_expand_group")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("gemm", t, flops=sum(2.0 * T * d * k + 2.0 * k * tr for k in ks),
+                    detail="grp" + "+".join(f"N{k}" for k in ks) + f"K{d}{'k' if w_kmajor else 'mn'}")
+    return ys
+
+
+def linear_dx_group(meta: PackMeta, dys, ws, a_shs, dhs, d: int, w_kmajor: bool = True,
+                    dx_out: torch.Tensor | None = None, dx_residual: torch.Tensor | None = None) -> torch.Tensor:
+    """K6 for targets sharing an input: dx = sum_j dy_j op(W_j)^T + dH_j A_j^T in ONE launch
+    (one fp32 accumulator over the concatenated K range)."""
+    T = dys[0].shape[0]
+    ks = [dy.shape[1] for dy in dys]
+    if dx_out is None:
+        dx_out = torch.empty((T, d), dtype=torch.bfloat16, device=dys[0].device)
+    karr = (ctypes.c_int64 * len(ks))(*ks)
+    t = _TIMER.start() if _TIMER else None
+    yp, _k1 = _ptr_array(dys, "dy")
+    wp, _k2 = _ptr_array(ws, "w")
+    ap, _k3 = _ptr_array(a_shs, "a_sh")
+    hp, _k4 = _ptr_array(dhs, "dh")
+    _lib.check(_lib.lib().plora_linear_dx_group(_stream(), ctypes.byref(meta.struct), len(dys), yp, karr, wp,
+                                                int(w_kmajor), ap, hp, d, _need(dx_out, "dx"), dx_out.stride(0),
+                                                _need(dx_residual, "dx_residual", allow_none=True)),
+               "plora_linear_dx_group")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("gemm", t, flops=sum(2.0 * T * d * k + 2.0 * d * tr for k in ks),
+                    detail="grp" + "+".join(f"K{k}" for k in ks) + f"N{d}{'mn' if w_kmajor else 'k'}")
+    return dx_out
+
+
 def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
                   bt_sh: torch.Tensor, hs: torch.Tensor, y_out: torch.Tensor | None = None,
                   residual: torch.Tensor | None = None) -> torch.Tensor:

@@ -198,3 +198,39 @@ def test_multi_target_shrink_and_segred_match_single(n_multi):
         ref = torch.full_like(gm, float("nan"))
         ops.segred(meta, x, q, ref)
         assert torch.equal(gm, ref)
+
+
+@pytest.mark.parametrize("kmajor", [True, False])
+def test_grouped_expand_and_dx_match_separate(kmajor):
+    """Grouped K1+K2b (N-segments, q/k/v-like widths incl. a narrow one) and grouped K6
+    (K-segments: one fp32 accumulator) vs separate launches / the fp32 reference."""
+    ranks = [8, 64, 16, 32, 8, 64, 1, 48]
+    tokens = [4096, 1024, 0, 2048, 333, 1024, 4096, 1500]
+    d = 1024
+    widths = [1024, 256, 512]
+    meta = build_meta(ranks, tokens, [float(r) for r in ranks]).to("cuda")
+    T, R64, n = meta.total_tokens, meta.rpad64, len(ranks)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(T, d, device="cuda", generator=g).to(bf)
+    ws = [((torch.randn(k, d, device="cuda", generator=g) if kmajor else torch.randn(d, k, device="cuda", generator=g))
+           * 0.03).to(bf) for k in widths]
+    bts = [(torch.randn(n, k, R64, device="cuda", generator=g) * 0.02).to(bf) for k in widths]
+    ats = [(torch.randn(n, d, R64, device="cuda", generator=g) * 0.02).to(bf) for _ in widths]
+    hss = [(torch.randn(T, R64, device="cuda", generator=g) * 0.5).to(bf) for _ in widths]
+    for h in hss:                                    # rank padding columns are zero in real packs
+        for i, r in enumerate(ranks):
+            h[meta.row_offsets[i]:meta.row_offsets[i + 1], r:] = 0
+    ys = ops.linear_expand_group(meta, x, ws, bts, hss, w_kmajor=kmajor)
+    for w, bt, hs, y in zip(ws, bts, hss, ys):
+        ref = ops.linear_expand(meta, x, w, kmajor, bt, hs)
+        assert torch.equal(y, ref)
+    dys = [(torch.randn(T, k, device="cuda", generator=g) * 0.1).to(bf) for k in widths]
+    dx = ops.linear_dx_group(meta, dys, ws, ats, hss, d, w_kmajor=kmajor)
+    want = torch.zeros(T, d, device="cuda")
+    for w, at, dh, dy in zip(ws, ats, hss, dys):
+        W = w.float().t() if kmajor else w.float()          # [d][k]
+        want += dy.float() @ W.t()
+        for i, r in enumerate(ranks):
+            s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+            want[s:e] += dh[s:e, :r].float() @ at[i, :, :r].float().t()
+    assert rel(dx, want) < 5e-3
