@@ -492,7 +492,7 @@ struct __align__(64) PairArgs {
   int32_t seg_nt_end[3];   // N-segments: cumulative n-tile counts
   int32_t seg_N[3];        // N-segments: valid output columns
   int32_t seg_kb_end[3];   // K-segments: cumulative main K-block counts
-  int32_t pad_;
+  int32_t band;            // tile raster: > 0 M-band row groups, < 0 N-band column tiles, 0 = kBand rows
   void* seg_out[3];        // N-segments: output base (masked direct stores)
   int64_t seg_ldo[3];
 };
@@ -509,13 +509,26 @@ template <int NB>
 __device__ __forceinline__ PairTile decode_pair_tile(const PairArgs& p, int idx) {
   const GemmArgs& a = p.g;
   PairTile t;
-  const int per_band = PairCfg<NB>::kBand * a.n_ntiles;
-  const int band = idx / per_band;
-  const int rem = idx - band * per_band;
-  const int g0 = band * PairCfg<NB>::kBand;
-  const int bsz = min(PairCfg<NB>::kBand, a.n_groups - g0);
-  const int nt = rem / bsz;
-  const int g = g0 + (rem - nt * bsz);
+  int g, nt;
+  if (p.band >= 0) {   // M-bands: `band` row groups, all column tiles, row group fastest
+    const int bw = p.band > 0 ? p.band : PairCfg<NB>::kBand;
+    const int per_band = bw * a.n_ntiles;
+    const int band = idx / per_band;
+    const int rem = idx - band * per_band;
+    const int g0 = band * bw;
+    const int bsz = min(bw, a.n_groups - g0);
+    nt = rem / bsz;
+    g = g0 + (rem - nt * bsz);
+  } else {             // N-bands: -band column tiles, all row groups, column tile fastest
+    const int bw = -p.band;
+    const int per_band = bw * a.n_groups;
+    const int band = idx / per_band;
+    const int rem = idx - band * per_band;
+    const int n0b = band * bw;
+    const int bsz = min(bw, a.n_ntiles - n0b);
+    g = rem / bsz;
+    nt = n0b + (rem - g * bsz);
+  }
   if (a.mtiles != nullptr) {
     const int4 mt = reinterpret_cast<const int4*>(a.mtiles)[g];
     t.m0 = mt.x;
