@@ -138,6 +138,9 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(const bf16* _
 }
 
 // dx = rstd * (g - xhat * mean(g * xhat)) (+ residual), g = dy * w, xhat = x * rstd.
+// All three row inputs (x, dy, residual) are loaded before the block reduction so their
+// latencies overlap; V = vectors of 8 per thread (d <= 2048 V).
+template <int V>
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* __restrict__ dy,
                                                                    const bf16* __restrict__ x,
                                                                    const float* __restrict__ rstd,
@@ -147,15 +150,16 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* _
   __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
   const float r = rstd[row];
-  float xh[kMaxV][8], g[kMaxV][8];
+  float xh[V][8], g[V][8], rf[V][8];
   float dot = 0.f;
 #pragma unroll
-  for (int j = 0; j < kMaxV; ++j) {
+  for (int j = 0; j < V; ++j) {
     const int c = (j * kNormThreads + threadIdx.x) * 8;
     if (c < d) {
       float wf[8], df[8];
       load8(x + row * d + c, xh[j]);
       load8(dy + row * d + c, df);
+      if (res) load8(res + row * d + c, rf[j]);
       load8(w + c, wf);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -167,13 +171,12 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* _
   }
   const float mean = block_sum<kNormThreads>(dot, red) / d;
 #pragma unroll
-  for (int j = 0; j < kMaxV; ++j) {
+  for (int j = 0; j < V; ++j) {
     const int c = (j * kNormThreads + threadIdx.x) * 8;
     if (c < d) {
-      float o[8], rf[8];
-      if (res) load8(res + row * d + c, rf);
+      float o[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = r * (g[j][e] - xh[j][e] * mean) + (res ? rf[e] : 0.f);
+      for (int e = 0; e < 8; ++e) o[e] = r * (g[j][e] - xh[j][e] * mean) + (res ? rf[j][e] : 0.f);
       store8(dx + row * d + c, o);
     }
   }
@@ -454,7 +457,9 @@ PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const voi
                                 const float* rstd, const void* w, const void* residual, void* dx) {
   if (d % 8 || d > 8 * kNormThreads * kMaxV) return plora::set_error("rmsnorm: d must be a multiple of 8, <= 8192");
   if (rows <= 0) return 0;
-  rmsnorm_bwd_kernel<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = d <= 8 * kNormThreads ? rmsnorm_bwd_kernel<1>
+            : (d <= 16 * kNormThreads ? rmsnorm_bwd_kernel<2> : rmsnorm_bwd_kernel<kMaxV>);
+  kern<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const bf16*>(dy), static_cast<const bf16*>(x), rstd, static_cast<const bf16*>(w),
       static_cast<const bf16*>(residual), static_cast<bf16*>(dx), (int)d);
   return launch_status("rmsnorm_bwd");
