@@ -152,6 +152,16 @@ PLORA_API int plora_linear_expand_group(void* stream, const plora_pack_t* pack,
                      const void* const* W, int32_t w_kmajor, const void* const* Bt_sh,
                      const void* const* Hs, void* const* Y);
 
+/* gate/up projections fused with the SwiGLU forward: one pair-GEMM launch whose tiles
+ * hold 256 gate and the same 256 up columns, so the epilogue writes
+ *   g = X W_gate^T + Hs_gate,i Bt_gate,i^T,  u = (same for up),  act = silu(g) u
+ * (act from the bf16-rounded g, u: bit-identical to plora_swiglu_fwd).  W_* nn.Linear
+ * layout [ffn][d]; g / u / act bf16 [T][ffn]. */
+PLORA_API int plora_linear_gate_up_swiglu(void* stream, const plora_pack_t* pack, const void* X,
+                     int64_t d, int64_t ffn, const void* W_gate, const void* W_up,
+                     const void* Bt_gate, const void* Bt_up, const void* Hs_gate, const void* Hs_up,
+                     void* g, void* u, void* act);
+
 /* Grouped K6 for those targets: dX [T][lddx] = sum_j dY[j] op(W[j])^T + dH[j]_i A_sh[j]_i^T
  * (+ dX_residual), one accumulator over the concatenated K range (K-segments). */
 PLORA_API int plora_linear_dx_group(void* stream, const plora_pack_t* pack, int32_t n,

@@ -32,6 +32,7 @@ EXPORTS = (
     "plora_linear_expand",
     "plora_linear_expand_group",
     "plora_linear_dx_group",
+    "plora_linear_gate_up_swiglu",
     "plora_linear_bwd",
     "plora_adamw",
     "plora_rmsnorm_fwd",
@@ -105,6 +106,7 @@ _SIGNATURES = {
                                    _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)], ctypes.c_int),
     "plora_linear_dx_group": ([_vp, ctypes.POINTER(PackStruct), _i32, ctypes.POINTER(_vp), _p64, ctypes.POINTER(_vp),
                                _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, _vp, _i64, _vp], ctypes.c_int),
+    "plora_linear_gate_up_swiglu": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64] + [_vp] * 9, ctypes.c_int),
     "plora_linear_bwd": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                           _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
     "plora_adamw": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _i64],

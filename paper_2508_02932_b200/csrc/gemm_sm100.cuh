@@ -493,9 +493,18 @@ struct __align__(64) PairArgs {
   int32_t seg_N[3];        // N-segments: valid output columns
   int32_t seg_kb_end[3];   // K-segments: cumulative main K-block counts
   int32_t band;            // tile raster: > 0 M-band row groups, < 0 N-band column tiles, 0 = kBand rows
+  int32_t paired;          // gate/up + SwiGLU: chunk c of every 256-column tile is segment c (see EPI_SWIGLU)
   void* seg_out[3];        // N-segments: output base (masked direct stores)
   int64_t seg_ldo[3];
 };
+
+// Epilogue variants of the pair kernel.
+//  EPI_STORE  : bf16 result (+ reduce-add) through TMA.
+//  EPI_SWIGLU : "paired" gate/up tiles -- TMEM columns [0,256) hold gate, [256,512) up for
+//               the same 256 ffn columns; the epilogue stores g, u (segments 0, 1) and
+//               act = silu(g) u (segment 2's map) computed from the bf16-rounded g, u,
+//               bit-identical to swiglu_fwd_kernel.
+enum PairEpi : int { EPI_STORE = 0, EPI_SWIGLU = 2 };
 
 __device__ __forceinline__ const CUtensorMap* seg_map(const CUtensorMap* m0, const CUtensorMap* rest, int s) {
   return s == 0 ? m0 : rest + (s - 1);
@@ -540,14 +549,19 @@ __device__ __forceinline__ PairTile decode_pair_tile(const PairArgs& p, int idx)
     t.adapter = 0;
   }
   int sg = 0;
-  while (sg + 1 < p.n_seg && nt >= p.seg_nt_end[sg]) ++sg;
-  t.seg = sg;
-  t.n0 = (nt - (sg ? p.seg_nt_end[sg - 1] : 0)) * PairCfg<NB>::kBN;
+  if (p.paired) {
+    t.seg = 0;
+    t.n0 = nt * 256;
+  } else {
+    while (sg + 1 < p.n_seg && nt >= p.seg_nt_end[sg]) ++sg;
+    t.seg = sg;
+    t.n0 = (nt - (sg ? p.seg_nt_end[sg - 1] : 0)) * PairCfg<NB>::kBN;
+  }
   t.n_main = p.seg_kb_end[p.k_seg - 1];
   if (a.has_lora) {
     t.rank = a.ranks[t.adapter];
     t.nlps = min((t.rank + 63) / 64, a.nb);
-    t.n_lora = t.nlps * p.k_seg;
+    t.n_lora = t.nlps * (p.paired ? 2 : p.k_seg);
   } else {
     t.rank = 0;
     t.nlps = 0;
@@ -609,7 +623,24 @@ __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg,
   }
 }
 
-template <bool B_MN, int NB>
+// EPI_SWIGLU: one gate chunk and the matching up chunk (bf16-packed) -> stores g, u and
+// act = silu(g) u from the bf16-rounded values (the arithmetic of swiglu_fwd_kernel).
+__device__ __forceinline__ void pair_emit_swiglu(const PairOut& pg, const PairOut& pu, const PairOut& pa, uint8_t* stg,
+                                                 int& issued, int lane, int col0, int m0, int m_len,
+                                                 const uint32_t (&vg)[16], const uint32_t (&vu)[16]) {
+  uint32_t va[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vg[q]));
+    const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vu[q]));
+    va[q] = pack_bf16x2(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+  }
+  pair_emit_chunk(pg, stg, issued, lane, col0, m0, m_len, vg);
+  pair_emit_chunk(pu, stg, issued, lane, col0, m0, m_len, vu);
+  pair_emit_chunk(pa, stg, issued, lane, col0, m0, m_len, va);
+}
+
+template <bool B_MN, int NB, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
     plora_gemm_pair_kernel(const __grid_constant__ PairArgs p) {
   using Cfg = PairCfg<NB>;
@@ -676,18 +707,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) mbar_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          const bool paired_lora = EPI == EPI_SWIGLU && b >= t.n_main;   // A + one B chunk
+          if (leader) mbar_expect_tx(&full_bar[stage], paired_lora ? 2 * (Cfg::kABytes + 16384) : 2 * Cfg::kStageBytes);
           const uint32_t fb = peer_masked(&full_bar[stage]);
           if (b < t.n_main) {
             int ks = 0;   // K-segment of this K-block
             while (ks + 1 < p.k_seg && b >= p.seg_kb_end[ks]) ++ks;
             const int kc = (b - (ks ? p.seg_kb_end[ks - 1] : 0)) * kBK;
             const CUtensorMap* mA = seg_map(&args.tmA, p.tmA2, ks);
-            const CUtensorMap* mB = seg_map(&args.tmB, p.tmB2, p.k_seg > 1 ? ks : t.seg);
             tma_load_2d_pair(sA, mA, fb, kc, t.m0 + half);
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
-              const int n = t.n0 + 256 * c + half;
+              // paired: chunk c is segment c (gate / up) at the same columns
+              const CUtensorMap* mB = seg_map(&args.tmB, p.tmB2, EPI == EPI_SWIGLU ? c : (p.k_seg > 1 ? ks : t.seg));
+              const int n = (EPI == EPI_SWIGLU ? t.n0 : t.n0 + 256 * c) + half;
               if (B_MN) {
                 tma_load_2d_pair(sB + c * 16384, mB, fb, n, kc);
                 tma_load_2d_pair(sB + c * 16384 + 8192, mB, fb, n + 64, kc);
@@ -697,13 +730,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
             }
           } else {
             const int lb = b - t.n_main;
-            const int ls = p.k_seg > 1 ? lb / t.nlps : t.seg;   // LoRA operands of this segment
-            const int lbs = p.k_seg > 1 ? lb - ls * t.nlps : lb;
+            const bool per_seg = p.k_seg > 1 || EPI == EPI_SWIGLU;
+            const int ls = per_seg ? lb / t.nlps : t.seg;   // LoRA operands of this segment
+            const int lbs = per_seg ? lb - ls * t.nlps : lb;
             tma_load_2d_pair(sA, seg_map(&args.tmH, p.tmH2, ls), fb, lbs * 64, t.m0 + half);
+            if (EPI == EPI_SWIGLU) {   // only chunk ls (gate or up) takes this LoRA block
+              tma_load_3d_pair(sB + ls * 16384, seg_map(&args.tmL, p.tmL2, ls), fb, lbs * 64, t.n0 + half, t.adapter);
+            } else {
 #pragma unroll
-            for (int c = 0; c < NB; ++c)
-              tma_load_3d_pair(sB + c * 16384, seg_map(&args.tmL, p.tmL2, ls), fb, lbs * 64, t.n0 + 256 * c + half,
-                               t.adapter);
+              for (int c = 0; c < NB; ++c)
+                tma_load_3d_pair(sB + c * 16384, seg_map(&args.tmL, p.tmL2, ls), fb, lbs * 64, t.n0 + 256 * c + half,
+                                 t.adapter);
+            }
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -733,12 +771,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
             const uint32_t a0 = smem_u32(sA);
             const uint32_t b0 = smem_u32(sB);
             const bool lora = b >= t.n_main;
-            const int lbs = lora ? (p.k_seg > 1 ? (b - t.n_main) % t.nlps : b - t.n_main) : 0;
+            const bool per_seg = p.k_seg > 1 || EPI == EPI_SWIGLU;
+            const int lbs = lora ? (per_seg ? (b - t.n_main) % t.nlps : b - t.n_main) : 0;
+            const int lchunk = (EPI == EPI_SWIGLU && lora) ? (b - t.n_main) / t.nlps : -1;
             const int ksteps = lora ? min(4, (t.rank - lbs * 64 + 15) / 16) : 4;
             for (int ks = 0; ks < ksteps; ++ks) {
               const uint64_t ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
 #pragma unroll
               for (int c = 0; c < NB; ++c) {
+                if (lchunk >= 0 && c != lchunk) continue;
                 uint64_t bd;
                 if (!lora && B_MN) bd = smem_desc_sw128(b0 + c * 16384 + ks * 2048, 8192, 1024);
                 else               bd = smem_desc_sw128(b0 + c * 16384 + ks * 32, 16, 1024);
@@ -778,6 +819,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     int acc = 0;
     uint32_t acc_phase = 0;
     int issued = 0;
+    if constexpr (EPI == EPI_SWIGLU) {
+      // paired gate/up tile: warp (quarter, chalf) owns gate chunks chalf*4+i (TMEM cols
+      // 0..255) and the matching up chunks 8+chalf*4+i; per pair it stores g, u and act.
+      constexpr int kPairs = 4, kDirectPairs = 3;
+      for (int idx = cluster; idx < total; idx += n_clusters) {
+        const PairTile t = decode_pair_tile<NB>(p, idx);
+        const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;
+        const int m_len = min(32, t.m_len - static_cast<int>(rank) * 128 - quarter * 32);
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
+        const bool store = m_len > 0;
+        PairOut pg, pu, pa;
+        pg.tm = &args.tmY;
+        pu.tm = &p.tmY2[0];
+        pa.tm = &p.tmY2[1];
+        pg.out = static_cast<__nv_bfloat16*>(p.seg_out[0]);
+        pu.out = static_cast<__nv_bfloat16*>(p.seg_out[1]);
+        pa.out = static_cast<__nv_bfloat16*>(p.seg_out[2]);
+        pg.ldo = pu.ldo = pa.ldo = p.seg_ldo[0];
+        pg.N = pu.N = pa.N = p.seg_N[0];
+        pg.accumulate = pu.accumulate = pa.accumulate = 0;
+        uint32_t kg[kPairs - kDirectPairs][16], ku[kPairs - kDirectPairs][16];
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) {
+          uint32_t r[32], vg[16], vu[16];
+          tmem_ld_32x32b_x32(tb + (chalf * 4 + i) * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) vg[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+          tmem_ld_32x32b_x32(tb + (8 + chalf * 4 + i) * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) vu[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+          if (i < kDirectPairs) {
+            if (store) pair_emit_swiglu(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len, vg, vu);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              kg[i - kDirectPairs][q] = vg[q];
+              ku[i - kDirectPairs][q] = vu[q];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);   // accumulator free: next mainloop
+        if (++acc == AS) { acc = 0; acc_phase ^= 1; }
+        if (!store) continue;
+#pragma unroll
+        for (int i = kDirectPairs; i < kPairs; ++i)
+          pair_emit_swiglu(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len,
+                           kg[i - kDirectPairs], ku[i - kDirectPairs]);
+      }
+    } else
     for (int idx = cluster; idx < total; idx += n_clusters) {
       const PairTile t = decode_pair_tile<NB>(p, idx);
       const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;   // this warp's 32 rows

@@ -164,9 +164,9 @@ static bool g_pair_enabled = [] {
   return !(e && e[0] == '0');
 }();
 
-template <bool B_MN, int NB>
+template <bool B_MN, int NB, int EPI = EPI_STORE>
 static int launch_pair(const PairArgs& args, cudaStream_t stream) {
-  auto kern = plora_gemm_pair_kernel<B_MN, NB>;
+  auto kern = plora_gemm_pair_kernel<B_MN, NB, EPI>;
   static bool configured = false;
   if (!configured) {
     PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<NB>::kSmemBytes));
@@ -210,7 +210,7 @@ struct PairSeg {
 
 // CTA-pair GEMM over 1..3 N-segments (shared A) or K-segments (shared output).
 static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t M, int n_seg, int k_seg,
-                             const PairSeg* sg, int w_kmajor, const void* residual) {
+                             const PairSeg* sg, int w_kmajor, const void* residual, void* swiglu_act = nullptr) {
   if (n_seg < 1 || k_seg < 1 || n_seg > 3 || k_seg > 3 || (n_seg > 1 && k_seg > 1))
     return fail("pair gemm: 1..3 N-segments or 1..3 K-segments");
   const int nseg = n_seg > k_seg ? n_seg : k_seg;
@@ -218,7 +218,10 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
   for (int s = 1; s < n_seg; ++s) Nmin = sg[s].N < Nmin ? sg[s].N : Nmin;
   int64_t Ntot = 0;
   for (int s = 0; s < n_seg; ++s) Ntot += sg[s].N;
-  const int NB = (n_seg > 1 ? Ntot : Nmin) >= g_pair_nb_min_n ? 2 : 1;
+  const bool paired = swiglu_act != nullptr;   // gate/up + SwiGLU (EPI_SWIGLU): segments 0, 1 share columns
+  if (paired && (n_seg != 2 || sg[0].N != sg[1].N || !w_kmajor || residual))
+    return fail("gate/up SwiGLU GEMM: two equal-width nn.Linear-layout segments");
+  const int NB = paired ? 2 : ((n_seg > 1 ? Ntot : Nmin) >= g_pair_nb_min_n ? 2 : 1);
   const int tile_n = 256 * NB;
   PairArgs pa;
   memset(&pa, 0, sizeof(pa));
@@ -254,7 +257,7 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
       pa.seg_out[s] = g.Y;
       pa.seg_ldo[s] = g.ldy;
       pa.seg_N[s] = static_cast<int>(N);
-      nt += static_cast<int>((N + tile_n - 1) / tile_n);
+      if (!paired || s == 0) nt += static_cast<int>((N + (paired ? 256 : tile_n) - 1) / (paired ? 256 : tile_n));
       pa.seg_nt_end[s] = nt;
     }
     if (s == 0 || k_seg > 1) {
@@ -264,6 +267,14 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
   }
   pa.n_seg = n_seg;
   pa.k_seg = k_seg;
+  if (paired) {   // act output: segment 2's output slot
+    if (reinterpret_cast<uintptr_t>(swiglu_act) % 16) return fail("gate/up SwiGLU GEMM: act must be 16-byte aligned");
+    if ((rc = make_map_out(mY[2], swiglu_act, sg[0].N, M, sg[0].ldy))) return rc;
+    pa.seg_out[2] = swiglu_act;
+    pa.seg_ldo[2] = sg[0].ldy;
+    pa.seg_N[2] = static_cast<int>(sg[0].N);
+    pa.paired = 1;
+  }
   if (lora) {
     a.ranks = pack->d_ranks;
     a.nb = pack->nb;
@@ -284,6 +295,7 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
   }
   a.debug = g_debug_flags;
   pa.band = g_pair_band;
+  if (paired) return launch_pair<false, 2, EPI_SWIGLU>(pa, st);
   if (NB == 2) return w_kmajor ? launch_pair<false, 2>(pa, st) : launch_pair<true, 2>(pa, st);
   return w_kmajor ? launch_pair<false, 1>(pa, st) : launch_pair<true, 1>(pa, st);
 }
@@ -655,6 +667,20 @@ int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void
   PairSeg sg[3];
   for (int j = 0; j < n; ++j) sg[j] = PairSeg{X, d, W[j], k_out[j], Hs[j], Bt_sh[j], Y[j], k_out[j]};
   return run_pair_segments(st, pack, T, n, 1, sg, w_kmajor, nullptr);
+}
+
+int plora_linear_gate_up_swiglu(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int64_t ffn,
+                                const void* W_gate, const void* W_up, const void* Bt_gate, const void* Bt_up,
+                                const void* Hs_gate, const void* Hs_up, void* g, void* u, void* act) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (!g || !u || !act) return fail("gate_up_swiglu: g, u and act are required");
+  const int64_t T = pack->total_tokens;
+  if (T <= 0) return 0;
+  if (!g_pair_enabled || (pack->d_ptiles == nullptr && pack->n_ptiles != 0) || ffn < 256)
+    return fail("gate_up_swiglu: needs the CTA-pair GEMM and ffn >= 256");
+  PairSeg sg[2] = {PairSeg{X, d, W_gate, ffn, Hs_gate, Bt_gate, g, ffn}, PairSeg{X, d, W_up, ffn, Hs_up, Bt_up, u, ffn}};
+  return run_pair_segments(static_cast<cudaStream_t>(stream), pack, T, 2, 1, sg, 1, nullptr, act);
 }
 
 int plora_linear_dx_group(void* stream, const plora_pack_t* pack, int32_t n, const void* const* dY,

@@ -23,6 +23,7 @@ recomputed.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -249,6 +250,7 @@ class PackedLoraTrainer:
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
         self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
+        self._fuse_swiglu = os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
@@ -360,10 +362,19 @@ class PackedLoraTrainer:
         self._reduce(o_out, hs_o)                      # row-parallel (TP): Y and Hs are partial sums
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
-        (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2)
+        if self._fuse_swiglu:   # gate/up GEMM with the SwiGLU forward in its epilogue
+            bank, meta = self.bank, self.meta
+            hs_g = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
+            hs_u = torch.empty_like(hs_g)
+            ops.shrink_multi(meta, x2, [bank.shadow_of(layer, "gate", "A"), bank.shadow_of(layer, "up", "A")],
+                             [hs_g, hs_u])
+            g, u, act = ops.linear_gate_up_swiglu(meta, x2, lw["gate"], lw["up"], bank.shadow_of(layer, "gate", "B"),
+                                                  bank.shadow_of(layer, "up", "B"), hs_g, hs_u)
+        else:
+            (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2)
+            act = ew.swiglu_fwd(g, u)
         x2_keep = x2 if self.save_normed else None
         del x2
-        act = ew.swiglu_fwd(g, u)
         d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
         self._reduce(d_out, hs_d)
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),

@@ -220,6 +220,27 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
     return ys
 
 
+def linear_gate_up_swiglu(meta: PackMeta, x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor,
+                          bt_gate: torch.Tensor, bt_up: torch.Tensor, hs_gate: torch.Tensor, hs_up: torch.Tensor):
+    """gate/up K1+K2b in one launch with the SwiGLU forward in the epilogue: returns
+    (g, u, act), act = silu(g) u bit-identical to elementwise.swiglu_fwd(g, u)."""
+    T, d = x.shape
+    ffn = w_gate.shape[0]
+    g = torch.empty((T, ffn), dtype=torch.bfloat16, device=x.device)
+    u = torch.empty_like(g)
+    act = torch.empty_like(g)
+    t = _TIMER.start() if _TIMER else None
+    _lib.check(_lib.lib().plora_linear_gate_up_swiglu(
+        _stream(), ctypes.byref(meta.struct), _need(x, "x"), d, ffn, _need(w_gate, "w_gate"), _need(w_up, "w_up"),
+        _need(bt_gate, "bt_gate"), _need(bt_up, "bt_up"), _need(hs_gate, "hs_gate"), _need(hs_up, "hs_up"),
+        _need(g, "g"), _need(u, "u"), _need(act, "act")), "plora_linear_gate_up_swiglu")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("gemm", t, flops=2 * (2.0 * T * d * ffn + 2.0 * ffn * tr), detail=f"gateup+swiglu N{ffn}K{d}k")
+    return g, u, act
+
+
 def linear_dx_group(meta: PackMeta, dys, ws, a_shs, dhs, d: int, w_kmajor: bool = True,
                     dx_out: torch.Tensor | None = None, dx_residual: torch.Tensor | None = None) -> torch.Tensor:
     """K6 for targets sharing an input: dx = sum_j dy_j op(W_j)^T + dH_j A_j^T in ONE launch

@@ -234,3 +234,28 @@ def test_grouped_expand_and_dx_match_separate(kmajor):
             s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
             want[s:e] += dh[s:e, :r].float() @ at[i, :, :r].float().t()
     assert rel(dx, want) < 5e-3
+
+
+@pytest.mark.parametrize("ffn", [1024, 1280, 1408])
+def test_gate_up_swiglu_fused_matches_unfused(ffn):
+    """gate/up K1+K2b with the SwiGLU forward in the epilogue == two grouped expands +
+    swiglu_fwd, bit for bit (ffn not a multiple of 512 / 256 exercises partial tiles)."""
+    from paper_2508_02932_b200 import elementwise as ew
+    ranks = [8, 64, 16, 32, 1]
+    tokens = [1024, 333, 2048, 0, 700]
+    d = 512
+    meta = build_meta(ranks, tokens, [2.0 * r for r in ranks]).to("cuda")
+    T, R64, n = meta.total_tokens, meta.rpad64, len(ranks)
+    g_ = torch.Generator(device="cuda").manual_seed(31)
+    x = torch.randn(T, d, device="cuda", generator=g_).to(bf)
+    wg, wu = [(torch.randn(ffn, d, device="cuda", generator=g_) * 0.05).to(bf) for _ in range(2)]
+    btg, btu = [(torch.randn(n, ffn, R64, device="cuda", generator=g_) * 0.05).to(bf) for _ in range(2)]
+    hsg, hsu = [(torch.randn(T, R64, device="cuda", generator=g_)).to(bf) for _ in range(2)]
+    for h in (hsg, hsu):
+        for i, r in enumerate(ranks):
+            h[meta.row_offsets[i]:meta.row_offsets[i + 1], r:] = 0
+    g, u, act = ops.linear_gate_up_swiglu(meta, x, wg, wu, btg, btu, hsg, hsu)
+    rg, ru = ops.linear_expand_group(meta, x, [wg, wu], [btg, btu], [hsg, hsu])
+    torch.cuda.synchronize()
+    assert torch.equal(g, rg) and torch.equal(u, ru)
+    assert torch.equal(act, ew.swiglu_fwd(rg, ru))
