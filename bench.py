@@ -182,6 +182,8 @@ def main() -> None:
     ap.add_argument("--tp", type=int, default=None,
                     help="tensor-parallel degree per packed job (config C4 default: all GPUs); "
                          "world/tp independent jobs run side by side")
+    ap.add_argument("--tp-comm", default="torch", choices=["torch", "abi"],
+                    help="TP all-reduce through torch.distributed (NCCL) or libplora's C-ABI (plora_tp_*, NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -195,7 +197,7 @@ def main() -> None:
     from paper_2508_02932_b200 import _lib, ops
     from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
 
-    from paper_2508_02932_b200.tp import DistComm
+    from paper_2508_02932_b200.tp import AbiNcclComm, DistComm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -214,7 +216,10 @@ def main() -> None:
     comm = None
     if tp > 1:   # one NCCL group per packed job (Megatron TP over NVLink), jobs side by side
         groups = [dist.new_group(list(range(j * tp, (j + 1) * tp))) for j in range(n_jobs)]
-        comm = DistComm(groups[job])
+        if args.tp_comm == "abi":
+            comm = AbiNcclComm(rank - job * tp, tp, group=groups[job])
+        else:
+            comm = DistComm(groups[job])
     specs, s = bench_adapters(args.config)
     n = len(specs)
     trainer = PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=[100 + i + 1000 * job for i in range(n)],

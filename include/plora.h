@@ -240,6 +240,22 @@ PLORA_API int plora_ce_stats(void* stream, int64_t rows, int64_t V, const void* 
 PLORA_API int plora_ce_apply(void* stream, int64_t rows, int64_t V, void* logits,
                              const int64_t* labels, int64_t v0, const float* lse, const float* weight);
 
+/* Tensor-parallel collectives of one packed job (config C4: the base is Megatron-sharded
+ * over NVLink; the LoRA-aware all-reduce placement is described in DESIGN.md section 7).
+ * NCCL is resolved at run time (dlopen of libnccl.so.2, reusing a copy already loaded in
+ * the process).  Rank 0 creates the id, the host distributes it to the group's ranks
+ * (any out-of-band channel), every rank calls plora_tp_comm_init.  All-reduce is in
+ * place on the caller's stream. */
+#define PLORA_TP_ID_BYTES 128
+#define PLORA_TP_BF16 0
+#define PLORA_TP_F32 1
+#define PLORA_TP_SUM 0
+#define PLORA_TP_MAX 1
+PLORA_API int plora_tp_get_unique_id(char* id_out /* PLORA_TP_ID_BYTES */);
+PLORA_API int plora_tp_comm_init(void** comm, const char* id, int32_t nranks, int32_t rank);
+PLORA_API int plora_tp_comm_destroy(void* comm);
+PLORA_API int plora_tp_allreduce(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t op);
+
 #ifdef __cplusplus
 }
 #endif

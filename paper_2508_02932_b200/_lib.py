@@ -44,6 +44,10 @@ EXPORTS = (
     "plora_cross_entropy",
     "plora_ce_stats",
     "plora_ce_apply",
+    "plora_tp_get_unique_id",
+    "plora_tp_comm_init",
+    "plora_tp_comm_destroy",
+    "plora_tp_allreduce",
 )
 
 ABI_VERSION = 4
@@ -121,6 +125,10 @@ _SIGNATURES = {
     "plora_cross_entropy": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp], ctypes.c_int),
     "plora_ce_stats": ([_vp, _i64, _i64, _vp, _vp, _i64, _vp], ctypes.c_int),
     "plora_ce_apply": ([_vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp], ctypes.c_int),
+    "plora_tp_get_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+    "plora_tp_comm_init": ([ctypes.POINTER(_vp), ctypes.c_char_p, _i32, _i32], ctypes.c_int),
+    "plora_tp_comm_destroy": ([_vp], ctypes.c_int),
+    "plora_tp_allreduce": ([_vp, _vp, _vp, _i64, _i32, _i32], ctypes.c_int),
 }
 
 

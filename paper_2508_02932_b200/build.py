@@ -12,7 +12,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libplora.so"
 
-SOURCES = ["plora_abi.cu", "adamw.cu", "elementwise.cu", "meta.cpp"]
+SOURCES = ["plora_abi.cu", "adamw.cu", "elementwise.cu", "meta.cpp", "tp_nccl.cpp"]
 HEADERS = ["sm100.cuh", "gemm_sm100.cuh"]
 
 NVCC_FLAGS = [

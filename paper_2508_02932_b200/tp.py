@@ -23,7 +23,8 @@ rank (identical inputs + deterministic kernels + all-reduced dH / Hs), so their
 AdamW states evolve identically without a gradient all-reduce.
 
 Communicators: ``DistComm`` wraps a torch.distributed process group (NCCL over
-NVLink/NVSwitch on the box; gloo in CPU tests).  ``ThreadComm`` runs a TP group
+NVLink/NVSwitch on the box; gloo in CPU tests); ``AbiNcclComm`` is the same NCCL
+all-reduce through libplora's C-ABI (``plora_tp_*``, for hosts without torch).  ``ThreadComm`` runs a TP group
 of g ranks as g threads sharing ONE GPU (each on its own stream) with a
 deterministic fixed-order sum -- it is how the sharded path is parity-tested on
 a single B200 (gpurun gives one GPU).
@@ -96,6 +97,48 @@ class DistComm(Comm):
         d = self._dist
         d.all_reduce(t, op=d.ReduceOp.SUM if op == "sum" else d.ReduceOp.MAX, group=self.group)
         return t
+
+
+class AbiNcclComm(Comm):
+    """The TP group's NCCL communicator created through libplora's C-ABI
+    (plora_tp_comm_init / plora_tp_allreduce) -- what a non-torch host uses.  ``group``
+    (a torch.distributed group) only carries the 128-byte NCCL id from rank 0; for a
+    one-rank group no process group is needed."""
+
+    _DT = {torch.bfloat16: 0, torch.float32: 1}
+
+    def __init__(self, rank: int = 0, world: int = 1, group=None):
+        import ctypes
+
+        from . import _lib
+
+        self._ct, self._lib = ctypes, _lib
+        self.rank, self.world = rank, world
+        idbuf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(_lib.lib().plora_tp_get_unique_id(idbuf), "plora_tp_get_unique_id")
+        if world > 1:
+            import torch.distributed as dist
+
+            obj = [idbuf.raw if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            idbuf = ctypes.create_string_buffer(obj[0], 128)
+        self._comm = ctypes.c_void_p()
+        _lib.check(_lib.lib().plora_tp_comm_init(ctypes.byref(self._comm), idbuf, world, rank), "plora_tp_comm_init")
+
+    def all_reduce_(self, t, op="sum"):
+        if t.dtype not in self._DT or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("tp all-reduce needs a contiguous CUDA bf16 / f32 tensor")
+        self._lib.check(self._lib.lib().plora_tp_allreduce(
+            torch.cuda.current_stream().cuda_stream, self._comm, t.data_ptr(), t.numel(), self._DT[t.dtype],
+            0 if op == "sum" else 1), "plora_tp_allreduce")
+        return t
+
+    def close(self):
+        if self._comm:
+            self._lib.check(self._lib.lib().plora_tp_comm_destroy(self._comm), "plora_tp_comm_destroy")
+            self._comm = self._ct.c_void_p()
 
 
 class _ThreadGroup:

@@ -113,3 +113,20 @@ def test_tp_shards_are_slices_of_unsharded_model():
                         assert torch.equal(tr.bank.block(tr.bank.P, layer, t.name, kind, i),
                                            ref.bank.block(ref.bank.P, layer, t.name, kind, i)[sl])
         assert torch.equal(tr.base.lm_head, ref.base.lm_head[sh.span(cfg.vocab)])
+
+
+def test_abi_nccl_comm_single_rank():
+    """The C-ABI TP collective (plora_tp_comm_init / plora_tp_allreduce over NCCL) on a
+    one-rank group: sum and max are the identity, bf16 and f32, on the current stream."""
+    from paper_2508_02932_b200.tp import AbiNcclComm
+    comm = AbiNcclComm()
+    try:
+        for dt in (torch.bfloat16, torch.float32):
+            x = torch.randn(4097, device="cuda").to(dt)
+            y = x.clone()
+            comm.all_reduce_(y)
+            comm.all_reduce_(y, "max")
+            torch.cuda.synchronize()
+            assert torch.equal(x, y)
+    finally:
+        comm.close()
