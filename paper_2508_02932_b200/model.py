@@ -250,7 +250,8 @@ class PackedLoraTrainer:
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
         self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
-        self._fuse_swiglu = os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
+        # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
+        self._fuse_swiglu = self.targets[4].h_out >= 256 and os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
