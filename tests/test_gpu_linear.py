@@ -174,11 +174,12 @@ def test_segred_lpt_schedule_matches_round_robin():
             assert rel(blk, ref) < 1e-4 if e > s else torch.equal(blk, torch.zeros_like(blk))
 
 
-@pytest.mark.parametrize("n_multi", [2, 3])
-def test_multi_target_shrink_and_segred_match_single(n_multi):
+@pytest.mark.parametrize("n_multi,big_rank", [(2, False), (3, False), (3, True)])
+def test_multi_target_shrink_and_segred_match_single(n_multi, big_rank):
     """K2a / K5 over targets sharing their input (q/k/v, gate/up) in one launch equal the
-    per-target launches bit for bit (same K order per output column)."""
-    ranks = [8, 64, 16, 32, 8, 64, 1, 48]
+    per-target launches bit for bit (same K order per output column); with a rank > 64
+    (two 64-column rank blocks) the entry points fall back to per-target launches."""
+    ranks = [8, 64, 16, 32, 8, 100 if big_rank else 64, 1, 48]
     tokens = [4096, 1024, 0, 2048, 333, 1024, 4096, 1500]
     d = 4096
     meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, 256, seed=5)
@@ -200,11 +201,12 @@ def test_multi_target_shrink_and_segred_match_single(n_multi):
         assert torch.equal(gm, ref)
 
 
-@pytest.mark.parametrize("kmajor", [True, False])
-def test_grouped_expand_and_dx_match_separate(kmajor):
+@pytest.mark.parametrize("kmajor,big_rank", [(True, False), (False, False), (True, True)])
+def test_grouped_expand_and_dx_match_separate(kmajor, big_rank):
     """Grouped K1+K2b (N-segments, q/k/v-like widths incl. a narrow one) and grouped K6
-    (K-segments: one fp32 accumulator) vs separate launches / the fp32 reference."""
-    ranks = [8, 64, 16, 32, 8, 64, 1, 48]
+    (K-segments: one fp32 accumulator) vs separate launches / the fp32 reference; a
+    rank > 64 adds a second LoRA K-block per segment."""
+    ranks = [8, 64, 16, 32, 8, 128 if big_rank else 64, 1, 48]
     tokens = [4096, 1024, 0, 2048, 333, 1024, 4096, 1500]
     d = 1024
     widths = [1024, 256, 512]

@@ -124,3 +124,27 @@ def test_saved_and_recomputed_norms_bit_identical():
     lb = b.forward_backward(tokens).clone()
     assert torch.equal(la, lb)
     assert torch.equal(a.bank.G, b.bank.G)
+
+
+def test_model_with_rank_above_64_matches_oracle():
+    """An adapter of rank 96 (two 64-column rank blocks in every shadow / Hs / dH) next to
+    small ranks, through the whole trainer, against the fp64 oracle decoder."""
+    from paper_2508_02932_b200.model import AdapterSpec
+    specs = [AdapterSpec(rank=96, alpha=48.0, batch=1, lr=1e-4), AdapterSpec(rank=8, alpha=16.0, batch=2, lr=2e-4),
+             AdapterSpec(rank=40, alpha=10.0, batch=1, lr=5e-5)]
+    tr = _trainer(specs=specs)
+    assert tr.meta.nb == 2
+    tokens = tr.synthetic_tokens().cuda()
+    losses = tr.forward_backward(tokens).cpu().double()
+    ref_losses, ref_grads, _ = _oracle(tr, tokens)
+    assert ((losses - ref_losses).abs() / ref_losses.abs()).max().item() <= 1e-2
+    num = den = 0.0
+    for (layer, tname), (dd, du) in ref_grads.items():
+        for i in range(tr.meta.n_adapters):
+            r = tr.meta.ranks[i]
+            ga = tr.bank.block(tr.bank.G, layer, tname, "A", i)[:, :r].double().cpu()
+            gb = tr.bank.block(tr.bank.G, layer, tname, "B", i)[:, :r].double().cpu().t()
+            for got, ref in ((ga, dd[i]), (gb, du[i])):
+                num += (got - ref).norm().item() ** 2
+                den += ref.norm().item() ** 2
+    assert (num / den) ** 0.5 <= 2e-2
