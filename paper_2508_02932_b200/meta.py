@@ -92,6 +92,45 @@ class PackMeta:
         self.device = device
         return self
 
+    def tile_chunks(self, n: int) -> list:
+        """Split the CTA-pair tile list into <= n contiguous token ranges at tile
+        boundaries: [(sub_meta, row_lo, row_hi)].  A sub_meta is this pack restricted to
+        those pair tiles -- pair-GEMM launches (N >= 256) with it write only rows
+        [row_lo, row_hi) of the full-size operands (used to overlap a tensor-parallel
+        all-reduce of one chunk with the GEMM of the next)."""
+        import copy
+
+        s = self.struct
+        key = ("chunks", n)
+        if key in self._dev:
+            return self._dev[key]
+        pt = self.ptiles
+        nt = pt.shape[0]
+        out = []
+        if nt == 0:
+            out = [(self, 0, self.total_tokens)]
+        else:
+            ends = np.cumsum(pt[:, 1].astype(np.int64))
+            cuts = [0]
+            for c in range(1, n):
+                j = int(np.searchsorted(ends, self.total_tokens * c / n))
+                if cuts[-1] < j < nt:
+                    cuts.append(j)
+            cuts.append(nt)
+            for lo, hi in zip(cuts[:-1], cuts[1:]):
+                sub = copy.copy(self)
+                st = _lib.PackStruct()
+                ctypes.pointer(st)[0] = s
+                st.d_ptiles = s.d_ptiles + lo * 16
+                st.n_ptiles = hi - lo
+                sub._struct = st
+                sub._dev = self._dev
+                if hasattr(sub, "_work"):
+                    del sub._work
+                out.append((sub, int(pt[lo, 0]), int(pt[hi - 1, 0] + pt[hi - 1, 1])))
+        self._dev[key] = out
+        return out
+
     @property
     def struct(self) -> _lib.PackStruct:
         if self._struct is None:

@@ -250,6 +250,8 @@ class PackedLoraTrainer:
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
         self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
+        self.tp_chunks = int(os.environ.get("PLORA_TP_CHUNKS", "4"))   # TP all-reduce / GEMM overlap depth
+        self._side = None
         # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
         self._fuse_swiglu = self.targets[4].h_out >= 256 and os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
@@ -278,6 +280,44 @@ class PackedLoraTrainer:
         y, hs = ops.linear_fwd(self.meta, x, w, True, a_sh, bt_sh, residual=residual)
         return y, hs
 
+    def _row_fwd(self, layer: int, tname: str, x: torch.Tensor, w: torch.Tensor):
+        """Row-parallel target (o, down).  Under TP the output Y_s = X_s W_s^T + Hs_s B^T is a
+        partial sum: its all-reduce runs per token chunk on a side stream, overlapping the
+        next chunk's GEMM; the partial Hs is all-reduced after the last chunk read it."""
+        if self.tp is None:
+            return self._lin_fwd(layer, tname, x, w)
+        bank, meta = self.bank, self.meta
+        hs = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
+        ops.shrink(meta, x, bank.shadow_of(layer, tname, "A"), hs)
+        y = torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device)
+        bt = bank.shadow_of(layer, tname, "B")
+        self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y), y, extra=(hs,))
+        return y, hs
+
+    def _overlapped(self, launch, y: torch.Tensor, extra=()):
+        """TP: enqueue launch(sub_pack) per token chunk of the pair-tile list on the current
+        stream and all-reduce that chunk's rows of y on the side stream as soon as its GEMM
+        is done (NCCL of chunk c overlaps the GEMM of chunk c+1); then all-reduce `extra`
+        there and make the current stream wait for the side stream."""
+        cur = torch.cuda.current_stream()
+        chunks = self.meta.tile_chunks(self.tp_chunks) if y.shape[1] >= 256 else [(self.meta, 0, self.T)]
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+        for sub, r0, r1 in chunks:
+            launch(sub)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                self.tp.all_reduce_(y[r0:r1])
+        with torch.cuda.stream(side):
+            for t in extra:
+                self.tp.all_reduce_(t)
+        done = torch.cuda.Event()
+        done.record(side)
+        cur.wait_event(done)
+
     def _lin_bwd(self, layer: int, tname: str, x, w, hs, dy, need_dx=True, dx_residual=None, dx_out=None):
         bank = self.bank
         return ops.linear_bwd(self.meta, x, w, True, bank.shadow_of(layer, tname, "A"),
@@ -299,8 +339,9 @@ class PackedLoraTrainer:
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
         """Backward of targets sharing the input x: per target K4 dH and K3 dB; ONE grouped
         K6 launch sums every target's input gradient in one fp32 accumulator; ONE K5
-        launch for every dA (x read once).  Column-parallel under TP: dH_s and dX_s are partial, dH is
-        all-reduced before dA (tp.py), dX by the caller."""
+        launch for every dA (x read once).  Column-parallel under TP: dH_s and dX_s are
+        partial -- both are all-reduced here (dX per token chunk, overlapping the GEMM),
+        dH before dA (tp.py)."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
         dhs = []
         for nm, hs, dy in zip(names, hss, dys):
@@ -309,10 +350,15 @@ class PackedLoraTrainer:
             ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, nm, "B"))              # K3 (Case 1)
             dhs.append(dh)
         dx = None
-        if need_dx:   # K6 (Case 4) for every target in one accumulator
-            dx = ops.linear_dx_group(meta, list(dys), [lw[nm] for nm in names],
-                                     [bank.shadow_of(layer, nm, "A") for nm in names], dhs, x.shape[1])
-        self._reduce(*dhs)
+        ws, ashs = [lw[nm] for nm in names], [bank.shadow_of(layer, nm, "A") for nm in names]
+        if need_dx and self.tp is not None:   # partial dX_s: chunked all-reduce overlapping the GEMM
+            dx = torch.empty((self.T, x.shape[1]), dtype=bf16, device=self.device)
+            self._overlapped(lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx),
+                             dx, extra=dhs)
+        else:
+            if need_dx:   # K6 (Case 4) for every target in one accumulator
+                dx = ops.linear_dx_group(meta, list(dys), ws, ashs, dhs, x.shape[1])
+            self._reduce(*dhs)
         ops.segred_multi(meta, x, dhs, [bank.region_flat(bank.G, layer, nm, "A") for nm in names])  # K5
         return dx
 
@@ -359,8 +405,7 @@ class PackedLoraTrainer:
         with torch.enable_grad():
             og = F.scaled_dot_product_attention(qg, kg, vg, is_causal=True, enable_gqa=(KV != H))
         attn = self._token_major(og.detach())                                           # [T][H*hd]
-        o_out, hs_o = self._lin_fwd(layer, "o", attn, lw["o"])
-        self._reduce(o_out, hs_o)                      # row-parallel (TP): Y and Hs are partial sums
+        o_out, hs_o = self._row_fwd(layer, "o", attn, lw["o"])   # TP: Y and Hs all-reduced (row-parallel)
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
         if self._fuse_swiglu:   # gate/up GEMM with the SwiGLU forward in its epilogue
@@ -376,8 +421,7 @@ class PackedLoraTrainer:
             act = ew.swiglu_fwd(g, u)
         x2_keep = x2 if self.save_normed else None
         del x2
-        d_out, hs_d = self._lin_fwd(layer, "down", act, lw["down"])
-        self._reduce(d_out, hs_d)
+        d_out, hs_d = self._row_fwd(layer, "down", act, lw["down"])
         save = _LayerSave(h_in=h, rstd1=rstd1, h_mid=h_mid, rstd2=rstd2, attn_graph=(qg, kg, vg, og),
                           attn_out=attn, g=g, u=u,
                           hs={"q": hs_q, "k": hs_k, "v": hs_v, "o": hs_o, "gate": hs_g, "up": hs_u, "down": hs_d},
@@ -405,7 +449,6 @@ class PackedLoraTrainer:
         x2 = sv.x2 if sv.x2 is not None else ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
         sv.x2 = None
         dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))
-        self._reduce(dx2)
         del dg, du, x2
         d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh, out=dx2)
         # attention: h_mid = h_in + o(attn(rope(q(x1)), rope(k(x1)), v(x1)))
@@ -423,7 +466,6 @@ class PackedLoraTrainer:
         del dq, dk, dv, x1
         if not need_dx:   # first layer: the embedding is frozen, no input gradient
             return None
-        self._reduce(dx1)
         return ew.rmsnorm_bwd(dx1, sv.h_in, sv.rstd1, lw["attn_norm"], residual_grad=d_mid, out=dx1)
 
     # ------------------------------------------------------------------ loss head
