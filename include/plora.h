@@ -255,6 +255,13 @@ PLORA_API int plora_tp_get_unique_id(char* id_out /* PLORA_TP_ID_BYTES */);
 PLORA_API int plora_tp_comm_init(void** comm, const char* id, int32_t nranks, int32_t rank);
 PLORA_API int plora_tp_comm_destroy(void* comm);
 PLORA_API int plora_tp_allreduce(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t op);
+/* Sequence-parallel pieces: recv[nranks * count] = concat of every rank's send[count];
+ * recv[recv_count] = sum over ranks of send[rank * recv_count ...]; buf on root = sum. */
+PLORA_API int plora_tp_allgather(void* stream, void* comm, const void* send, void* recv, int64_t count,
+                                 int32_t dtype);
+PLORA_API int plora_tp_reducescatter(void* stream, void* comm, const void* send, void* recv, int64_t recv_count,
+                                     int32_t dtype);
+PLORA_API int plora_tp_reduce(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t root);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,9 @@ EXPORTS = (
     "plora_tp_comm_init",
     "plora_tp_comm_destroy",
     "plora_tp_allreduce",
+    "plora_tp_allgather",
+    "plora_tp_reducescatter",
+    "plora_tp_reduce",
 )
 
 ABI_VERSION = 4
@@ -129,6 +132,9 @@ _SIGNATURES = {
     "plora_tp_comm_init": ([ctypes.POINTER(_vp), ctypes.c_char_p, _i32, _i32], ctypes.c_int),
     "plora_tp_comm_destroy": ([_vp], ctypes.c_int),
     "plora_tp_allreduce": ([_vp, _vp, _vp, _i64, _i32, _i32], ctypes.c_int),
+    "plora_tp_allgather": ([_vp, _vp, _vp, _vp, _i64, _i32], ctypes.c_int),
+    "plora_tp_reducescatter": ([_vp, _vp, _vp, _vp, _i64, _i32], ctypes.c_int),
+    "plora_tp_reduce": ([_vp, _vp, _vp, _i64, _i32, _i32], ctypes.c_int),
 }
 
 

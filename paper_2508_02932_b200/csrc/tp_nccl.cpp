@@ -29,6 +29,11 @@ struct NcclApi {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                 cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   bool ok = false;
 };
 
@@ -45,13 +50,25 @@ const NcclApi& api() {
     a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_reduce && a.error_string;
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.reduce_scatter = reinterpret_cast<decltype(a.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
+    a.reduce = reinterpret_cast<decltype(a.reduce)>(dlsym(h, "ncclReduce"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_reduce && a.error_string &&
+           a.all_gather && a.reduce_scatter && a.reduce;
   });
   return a;
 }
 
 int nccl_fail(const char* what, ncclResult_t r) {
   return plora::set_error(std::string(what) + ": " + api().error_string(r));
+}
+
+int nccl_dtype(int32_t dtype, ncclDataType_t* dt) {
+  switch (dtype) {
+    case PLORA_TP_BF16: *dt = ncclBfloat16; return 0;
+    case PLORA_TP_F32: *dt = ncclFloat32; return 0;
+    default: return plora::set_error("tp: dtype must be PLORA_TP_BF16 or PLORA_TP_F32");
+  }
 }
 
 }  // namespace
@@ -113,6 +130,44 @@ PLORA_API int plora_tp_allreduce(void* stream, void* comm, void* buf, int64_t co
   const ncclResult_t r = a.all_reduce(buf, buf, static_cast<size_t>(count), dt, ro, static_cast<ncclComm_t>(comm),
                                       static_cast<cudaStream_t>(stream));
   return r == ncclSuccess ? 0 : nccl_fail("ncclAllReduce", r);
+}
+
+PLORA_API int plora_tp_allgather(void* stream, void* comm, const void* send, void* recv, int64_t count,
+                                 int32_t dtype) {
+  const NcclApi& a = api();
+  if (!a.ok) return plora::set_error("tp: libnccl.so.2 not available");
+  if (!comm) return plora::set_error("tp: comm is NULL");
+  if (count <= 0) return count == 0 ? 0 : plora::set_error("tp: negative count");
+  ncclDataType_t dt;
+  if (nccl_dtype(dtype, &dt)) return 1;
+  const ncclResult_t r = a.all_gather(send, recv, static_cast<size_t>(count), dt, static_cast<ncclComm_t>(comm),
+                                      static_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? 0 : nccl_fail("ncclAllGather", r);
+}
+
+PLORA_API int plora_tp_reducescatter(void* stream, void* comm, const void* send, void* recv, int64_t recv_count,
+                                     int32_t dtype) {
+  const NcclApi& a = api();
+  if (!a.ok) return plora::set_error("tp: libnccl.so.2 not available");
+  if (!comm) return plora::set_error("tp: comm is NULL");
+  if (recv_count <= 0) return recv_count == 0 ? 0 : plora::set_error("tp: negative count");
+  ncclDataType_t dt;
+  if (nccl_dtype(dtype, &dt)) return 1;
+  const ncclResult_t r = a.reduce_scatter(send, recv, static_cast<size_t>(recv_count), dt, ncclSum,
+                                          static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? 0 : nccl_fail("ncclReduceScatter", r);
+}
+
+PLORA_API int plora_tp_reduce(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t root) {
+  const NcclApi& a = api();
+  if (!a.ok) return plora::set_error("tp: libnccl.so.2 not available");
+  if (!comm) return plora::set_error("tp: comm is NULL");
+  if (count <= 0) return count == 0 ? 0 : plora::set_error("tp: negative count");
+  ncclDataType_t dt;
+  if (nccl_dtype(dtype, &dt)) return 1;
+  const ncclResult_t r = a.reduce(buf, buf, static_cast<size_t>(count), dt, ncclSum, root,
+                                  static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? 0 : nccl_fail("ncclReduce", r);
 }
 
 }  // extern "C"

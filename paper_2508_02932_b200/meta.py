@@ -98,9 +98,7 @@ class PackMeta:
         those pair tiles -- pair-GEMM launches (N >= 256) with it write only rows
         [row_lo, row_hi) of the full-size operands (used to overlap a tensor-parallel
         all-reduce of one chunk with the GEMM of the next)."""
-        import copy
-
-        s = self.struct
+        self.struct   # uploaded
         key = ("chunks", n)
         if key in self._dev:
             return self._dev[key]
@@ -118,18 +116,50 @@ class PackMeta:
                     cuts.append(j)
             cuts.append(nt)
             for lo, hi in zip(cuts[:-1], cuts[1:]):
-                sub = copy.copy(self)
-                st = _lib.PackStruct()
-                ctypes.pointer(st)[0] = s
-                st.d_ptiles = s.d_ptiles + lo * 16
-                st.n_ptiles = hi - lo
-                sub._struct = st
-                sub._dev = self._dev
-                if hasattr(sub, "_work"):
-                    del sub._work
-                out.append((sub, int(pt[lo, 0]), int(pt[hi - 1, 0] + pt[hi - 1, 1])))
+                out.append((self._sub(lo, hi), int(pt[lo, 0]), int(pt[hi - 1, 0] + pt[hi - 1, 1])))
         self._dev[key] = out
         return out
+
+    def shard_tile_chunks(self, world: int):
+        """The pair-tile list cut exactly at the sequence-parallel shard boundaries
+        (rows r * T / world): [(sub_meta, row_lo, row_hi)] per shard, or None when a
+        boundary falls inside a pair tile (T not divisible, or unaligned segments)."""
+        key = ("shard_chunks", world)
+        if key in self._dev:
+            return self._dev[key]
+        T = self.total_tokens
+        out = None
+        if T % world == 0 and self.ptiles.shape[0] > 0:
+            starts = self.ptiles[:, 0].astype(np.int64)
+            cuts = [0]
+            for r in range(1, world):
+                j = np.flatnonzero(starts == r * (T // world))
+                if j.size == 0:
+                    cuts = None
+                    break
+                cuts.append(int(j[0]))
+            if cuts is not None:
+                cuts.append(self.ptiles.shape[0])
+                out = [(self._sub(lo, hi), r * (T // world), (r + 1) * (T // world))
+                       for r, (lo, hi) in enumerate(zip(cuts[:-1], cuts[1:]))]
+        self._dev[key] = out
+        return out
+
+    def _sub(self, lo: int, hi: int) -> "PackMeta":
+        """This pack restricted to pair tiles [lo, hi) (pair-GEMM launches only)."""
+        import copy
+
+        s = self.struct
+        sub = copy.copy(self)
+        st = _lib.PackStruct()
+        ctypes.pointer(st)[0] = s
+        st.d_ptiles = s.d_ptiles + lo * 16
+        st.n_ptiles = hi - lo
+        sub._struct = st
+        sub._dev = self._dev
+        if hasattr(sub, "_work"):
+            del sub._work
+        return sub
 
     @property
     def struct(self) -> _lib.PackStruct:

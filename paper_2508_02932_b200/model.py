@@ -211,7 +211,7 @@ class PackedLoraTrainer:
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
-                 save_normed: bool | None = None):
+                 save_normed: bool | None = None, sequence_parallel: bool = True):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the all-reduces described in tp.py."""
@@ -231,6 +231,12 @@ class PackedLoraTrainer:
         self.meta: PackMeta = build_meta([sp.rank for sp in specs], tokens, [sp.alpha for sp in specs]).to(
             self.device)
         self.T = self.meta.total_tokens
+        # Megatron sequence parallelism under TP: the residual stream, norms and their saved
+        # activations hold only this rank's T/tp token rows; all-gather before the column-
+        # parallel projections, reduce-scatter after the row-parallel ones (tp.py)
+        self.sp = self.tp is not None and sequence_parallel and self.T % g == 0
+        self.Tl = self.T // g if self.sp else self.T
+        self.r0 = self.shard.rank * self.Tl if self.sp else 0
         self.base = base or BaseWeights(cfg, self.device, shard=self.shard)
         if self.base.shard != self.shard:
             raise ValueError("base weights are sharded for a different tensor-parallel position")
@@ -262,7 +268,7 @@ class PackedLoraTrainer:
         attention output, gate/up and the 7 Hs tiles (+ the two normed inputs)."""
         cfg, T, hd = self.cfg, self.T, self.cfg.head_dim
         ffn_l = self.targets[4].h_out
-        per = (2 * cfg.d + (self.H_l + 2 * self.KV_l) * hd + self.H_l * hd + 2 * ffn_l
+        per = (2 * cfg.d * self.Tl // T + (self.H_l + 2 * self.KV_l) * hd + self.H_l * hd + 2 * ffn_l
                + 7 * self.meta.rpad64 + (2 * cfg.d if save_normed else 0))
         return 2 * T * per * cfg.n_layers
 
@@ -291,32 +297,67 @@ class PackedLoraTrainer:
         ops.shrink(meta, x, bank.shadow_of(layer, tname, "A"), hs)
         y = torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device)
         bt = bank.shadow_of(layer, tname, "B")
-        self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y), y, extra=(hs,))
+        y = self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y), y, extra=(hs,))
         return y, hs
 
     def _overlapped(self, launch, y: torch.Tensor, extra=()):
         """TP: enqueue launch(sub_pack) per token chunk of the pair-tile list on the current
-        stream and all-reduce that chunk's rows of y on the side stream as soon as its GEMM
-        is done (NCCL of chunk c overlaps the GEMM of chunk c+1); then all-reduce `extra`
-        there and make the current stream wait for the side stream."""
+        stream and reduce that chunk's rows of the partial y on the side stream as soon as
+        its GEMM is done (NCCL of chunk c overlaps the GEMM of chunk c+1); then all-reduce
+        `extra` there and make the current stream wait for the side stream.
+        Without sequence parallelism the chunks are all-reduced and y is returned; with it
+        the chunks are the ranks' token shards, each reduced onto its owner (ncclReduce),
+        and this rank's [T/tp][d] shard of the sum is returned (a view of y) -- or, when a
+        shard boundary falls inside a pair tile, one GEMM then a reduce-scatter."""
         cur = torch.cuda.current_stream()
-        chunks = self.meta.tile_chunks(self.tp_chunks) if y.shape[1] >= 256 else [(self.meta, 0, self.T)]
         if self._side is None:
             self._side = torch.cuda.Stream(device=self.device)
         side = self._side
-        for sub, r0, r1 in chunks:
-            launch(sub)
-            ev = torch.cuda.Event()
-            ev.record(cur)
-            side.wait_event(ev)
-            with torch.cuda.stream(side):
-                self.tp.all_reduce_(y[r0:r1])
+        wide = y.shape[1] >= 256   # pair-GEMM path (sub-packs only restrict pair tiles)
+        out = y
+        if self.sp:
+            chunks = self.meta.shard_tile_chunks(self.shard.world) if wide else None
+            if chunks is None:
+                launch(self.meta)
+                out = torch.empty((self.Tl, y.shape[1]), dtype=y.dtype, device=y.device)
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    self.tp.reduce_scatter_(out, y)
+            else:
+                for owner, (sub, r0, r1) in enumerate(chunks):
+                    launch(sub)
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    side.wait_event(ev)
+                    with torch.cuda.stream(side):
+                        self.tp.reduce_(y[r0:r1], owner)
+                out = y[self.r0:self.r0 + self.Tl]
+        else:
+            chunks = self.meta.tile_chunks(self.tp_chunks) if wide else [(self.meta, 0, self.T)]
+            for sub, r0, r1 in chunks:
+                launch(sub)
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    self.tp.all_reduce_(y[r0:r1])
         with torch.cuda.stream(side):
             for t in extra:
                 self.tp.all_reduce_(t)
         done = torch.cuda.Event()
         done.record(side)
         cur.wait_event(done)
+        return out
+
+    def _gather(self, x_s: torch.Tensor) -> torch.Tensor:
+        """Sequence parallelism: every rank's [T/tp][d] token shard -> the full [T][d]."""
+        if not self.sp:
+            return x_s
+        full = torch.empty((self.T, x_s.shape[1]), dtype=x_s.dtype, device=x_s.device)
+        self.tp.all_gather_(full, x_s)
+        return full
 
     def _lin_bwd(self, layer: int, tname: str, x, w, hs, dy, need_dx=True, dx_residual=None, dx_out=None):
         bank = self.bank
@@ -353,8 +394,8 @@ class PackedLoraTrainer:
         ws, ashs = [lw[nm] for nm in names], [bank.shadow_of(layer, nm, "A") for nm in names]
         if need_dx and self.tp is not None:   # partial dX_s: chunked all-reduce overlapping the GEMM
             dx = torch.empty((self.T, x.shape[1]), dtype=bf16, device=self.device)
-            self._overlapped(lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx),
-                             dx, extra=dhs)
+            dx = self._overlapped(lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx),
+                                  dx, extra=dhs)
         else:
             if need_dx:   # K6 (Case 4) for every target in one accumulator
                 dx = ops.linear_dx_group(meta, list(dys), ws, ashs, dhs, x.shape[1])
@@ -390,6 +431,7 @@ class PackedLoraTrainer:
             x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
         else:
             h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
+        x1 = self._gather(x1)     # sequence parallel: the rank's token shard -> all T rows
         (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1)
         x1_keep = x1 if self.save_normed else None
         del x1
@@ -408,6 +450,7 @@ class PackedLoraTrainer:
         o_out, hs_o = self._row_fwd(layer, "o", attn, lw["o"])   # TP: Y and Hs all-reduced (row-parallel)
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
+        x2 = self._gather(x2)
         if self._fuse_swiglu:   # gate/up GEMM with the SwiGLU forward in its epilogue
             bank, meta = self.bank, self.meta
             hs_g = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
@@ -437,29 +480,32 @@ class PackedLoraTrainer:
         # Cases 2/1/4 run first; the SwiGLU backward re-emits the activation in the same
         # pass (no separate recompute), then Case 3 dA_down = act^T dH.
         bank, meta = self.bank, self.meta
+        dh_s = dh
+        dh = self._gather(dh_s)   # sequence parallel: the row-parallel output gradient on all T rows
         dh_down = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
         ops.shrink(meta, dh, bank.shadow_of(layer, "down", "B"), dh_down)                     # K4
         ops.segred(meta, dh, sv.hs["down"], bank.region_flat(bank.G, layer, "down", "B"))    # K3
         d_act = ops.linear_expand(meta, dh, lw["down"], False, bank.shadow_of(layer, "down", "A"), dh_down)  # K6
+        del dh
         act = torch.empty_like(sv.g)
         dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u, act_out=act)  # in place over g, u
         del d_act
         ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
         del act, dh_down
-        x2 = sv.x2 if sv.x2 is not None else ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"])
+        x2 = sv.x2 if sv.x2 is not None else self._gather(ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"]))
         sv.x2 = None
         dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))
         del dg, du, x2
-        d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh, out=dx2)
+        d_mid = ew.rmsnorm_bwd(dx2, sv.h_mid, sv.rstd2, lw["mlp_norm"], residual_grad=dh_s, out=dx2)
         # attention: h_mid = h_in + o(attn(rope(q(x1)), rope(k(x1)), v(x1)))
-        d_attn = self._lin_bwd(layer, "o", sv.attn_out, lw["o"], sv.hs["o"], d_mid)
+        d_attn = self._lin_bwd(layer, "o", sv.attn_out, lw["o"], sv.hs["o"], self._gather(d_mid))
         qg, kg, vg, og = sv.attn_graph
         dq, dk, dv = torch.autograd.grad(og, (qg, kg, vg), d_attn.view(B, s, H, hd).transpose(1, 2))
         del d_attn
         dq = ew.rope(dq.transpose(1, 2), self.cos, self.sin, s, inverse=True)      # [T][H*hd]
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
         dv = self._token_major(dv)
-        x1 = sv.x1 if sv.x1 is not None else ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"])
+        x1 = sv.x1 if sv.x1 is not None else self._gather(ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"]))
         sv.x1 = None
         dx1 = self._group_bwd(layer, ("v", "k", "q"), x1, (sv.hs["v"], sv.hs["k"], sv.hs["q"]), (dv, dk, dq),
                               need_dx=need_dx)
@@ -474,6 +520,7 @@ class PackedLoraTrainer:
         d h.  Writes per-adapter losses into self.losses."""
         cfg = self.cfg
         h, xf, rstd = ew.add_rmsnorm_fwd(h_prev, delta, self.base.final_norm, cfg.norm_eps)
+        xf = self._gather(xf)
         dxf = torch.empty_like(xf)
         labels = torch.roll(tokens, -1)
         tok_loss = torch.empty(self.T, dtype=torch.float32, device=self.device)
@@ -495,7 +542,12 @@ class PackedLoraTrainer:
                 tok_loss[c0:c1] = w * (lse - sl[:, 1])
             ops.gemm(logits, self.base.lm_head, False, out=dxf[c0:c1])   # dX = dlogits @ W_lm
             del logits
-        self._reduce(dxf)
+        if self.sp:   # partial over the vocabulary shards -> this rank's token shard of the sum
+            dxf_s = torch.empty((self.Tl, dxf.shape[1]), dtype=bf16, device=self.device)
+            self.tp.reduce_scatter_(dxf_s, dxf)
+            dxf = dxf_s
+        else:
+            self._reduce(dxf)
         # per-adapter sums over contiguous segments (deterministic prefix-sum differences)
         cs = torch.cumsum(tok_loss.double(), 0)
         cs = torch.cat((cs.new_zeros(1), cs))
@@ -506,7 +558,7 @@ class PackedLoraTrainer:
     # ------------------------------------------------------------------ step
     def forward_backward(self, tokens: torch.Tensor) -> torch.Tensor:
         """Full packed forward + backward; fills bank.G; returns per-adapter losses (device)."""
-        h = self.base.embed[tokens]
+        h = self.base.embed[tokens[self.r0:self.r0 + self.Tl]]   # sequence parallel: own token rows
         delta = None
         saves = []
         for layer in range(self.cfg.n_layers):

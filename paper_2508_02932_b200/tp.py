@@ -74,11 +74,24 @@ class TPShard:
 
 
 class Comm:
-    """Minimal collective interface the TP trainer needs (in-place all-reduce)."""
+    """Collective interface the TP trainer needs.  Tensors are contiguous; in place.
+      all_reduce_(t)           t = sum_r t_r (or max)
+      all_gather_(out, inp)    out = concat_r inp_r (rank order, along dim 0)
+      reduce_scatter_(out, inp) out = sum_r inp_r[rank block]
+      reduce_(t, root)         t on `root` = sum_r t_r (other ranks: unspecified)"""
     rank: int = 0
     world: int = 1
 
     def all_reduce_(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+    def all_gather_(self, out: torch.Tensor, inp: torch.Tensor) -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+    def reduce_scatter_(self, out: torch.Tensor, inp: torch.Tensor) -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+    def reduce_(self, t: torch.Tensor, root: int) -> torch.Tensor:  # pragma: no cover
         raise NotImplementedError
 
 
@@ -96,6 +109,19 @@ class DistComm(Comm):
     def all_reduce_(self, t, op="sum"):
         d = self._dist
         d.all_reduce(t, op=d.ReduceOp.SUM if op == "sum" else d.ReduceOp.MAX, group=self.group)
+        return t
+
+    def all_gather_(self, out, inp):
+        self._dist.all_gather_into_tensor(out, inp, group=self.group)
+        return out
+
+    def reduce_scatter_(self, out, inp):
+        self._dist.reduce_scatter_tensor(out, inp, group=self.group)
+        return out
+
+    def reduce_(self, t, root):
+        d = self._dist
+        d.reduce(t, dst=d.get_global_rank(self.group, root) if self.group is not None else root, group=self.group)
         return t
 
 
@@ -135,6 +161,32 @@ class AbiNcclComm(Comm):
             0 if op == "sum" else 1), "plora_tp_allreduce")
         return t
 
+    def all_gather_(self, out, inp):
+        self._check(out, inp)
+        self._lib.check(self._lib.lib().plora_tp_allgather(
+            torch.cuda.current_stream().cuda_stream, self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
+            self._DT[inp.dtype]), "plora_tp_allgather")
+        return out
+
+    def reduce_scatter_(self, out, inp):
+        self._check(out, inp)
+        self._lib.check(self._lib.lib().plora_tp_reducescatter(
+            torch.cuda.current_stream().cuda_stream, self._comm, inp.data_ptr(), out.data_ptr(), out.numel(),
+            self._DT[inp.dtype]), "plora_tp_reducescatter")
+        return out
+
+    def reduce_(self, t, root):
+        self._check(t)
+        self._lib.check(self._lib.lib().plora_tp_reduce(
+            torch.cuda.current_stream().cuda_stream, self._comm, t.data_ptr(), t.numel(), self._DT[t.dtype], root),
+            "plora_tp_reduce")
+        return t
+
+    def _check(self, *ts):
+        for t in ts:
+            if t.dtype not in self._DT or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("tp collectives need contiguous CUDA bf16 / f32 tensors")
+
     def close(self):
         if self._comm:
             self._lib.check(self._lib.lib().plora_tp_comm_destroy(self._comm), "plora_tp_comm_destroy")
@@ -160,25 +212,47 @@ class ThreadComm(Comm):
         self.rank = rank
         self.world = group.world
 
-    def all_reduce_(self, t, op="sum"):
+    def _exchange(self, t, combine, deliver):
+        """Every rank deposits t; rank 0 computes combine(slots) (fp32, fixed rank order);
+        every rank then runs deliver(result)."""
         g = self.g
         if t.is_cuda:
             torch.cuda.current_stream().synchronize()
         g.slots[self.rank] = t
         g.barrier.wait()
         if self.rank == 0:
-            acc = g.slots[0].float().clone()
-            for other in g.slots[1:]:
-                o = other.float()
-                acc = acc + o if op == "sum" else torch.maximum(acc, o)
-            g.result = acc
+            g.result = combine(g.slots)
             if t.is_cuda:
                 torch.cuda.current_stream().synchronize()
         g.barrier.wait()
-        t.copy_(g.result)
+        deliver(g.result)
         if t.is_cuda:
             torch.cuda.current_stream().synchronize()
         g.barrier.wait()   # everyone has read the result before any rank deposits again
+
+    @staticmethod
+    def _sum(slots, op="sum"):
+        acc = slots[0].float().clone()
+        for other in slots[1:]:
+            o = other.float()
+            acc = acc + o if op == "sum" else torch.maximum(acc, o)
+        return acc
+
+    def all_reduce_(self, t, op="sum"):
+        self._exchange(t, lambda sl: self._sum(sl, op), t.copy_)
+        return t
+
+    def all_gather_(self, out, inp):
+        self._exchange(inp, lambda sl: torch.cat([x.clone() for x in sl], 0), out.copy_)
+        return out
+
+    def reduce_scatter_(self, out, inp):
+        n = out.shape[0]
+        self._exchange(inp, self._sum, lambda r: out.copy_(r[self.rank * n:(self.rank + 1) * n]))
+        return out
+
+    def reduce_(self, t, root):
+        self._exchange(t, self._sum, lambda r: t.copy_(r) if self.rank == root else None)
         return t
 
 

@@ -19,11 +19,11 @@ from paper_2508_02932_b200.tp import TPShard, run_threaded
 pytestmark = pytest.mark.gpu
 
 
-def _make(preset, tp=None):
+def _make(preset, tp=None, sp=True):
     cfg = PRESETS[preset]
     specs, s = bench_adapters(preset)
     return PackedLoraTrainer(cfg, specs, s, device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in specs],
-                             tp=tp)
+                             tp=tp, sequence_parallel=sp)
 
 
 def _grads(tr):
@@ -45,15 +45,20 @@ def _masters(tr):
             for i in range(tr.meta.n_adapters)}
 
 
-@pytest.mark.parametrize("preset,g", [("tiny-qwen", 2), ("tiny", 4)])
-def test_tp_matches_unsharded(preset, g):
+@pytest.mark.parametrize("preset,g,sp", [("tiny-qwen", 2, True), ("tiny", 4, True), ("tiny-qwen", 2, False),
+                                         ("tiny", 4, False)])
+def test_tp_matches_unsharded(preset, g, sp):
+    """sp: Megatron sequence parallelism (token-sharded residual stream; g = 2 cuts the
+    pair-tile list exactly at the shard boundaries -> per-shard reduces overlapping the
+    GEMM; g = 4 does not -> one reduce-scatter); sp = False: all-reduce chunks."""
     ref = _make(preset)
     tokens = ref.synthetic_tokens().cuda()
     ref_losses = ref.forward_backward(tokens).double().cpu()
     ref_grads = _grads(ref)
 
     def rank_fn(comm):
-        tr = _make(preset, tp=comm)
+        tr = _make(preset, tp=comm, sp=sp)
+        assert tr.sp == sp
         losses = tr.forward_backward(tokens).double().cpu()
         grads = _grads(tr)
         tr.bank.adamw_step()
@@ -85,7 +90,7 @@ def test_tp_matches_unsharded(preset, g):
         num += e * e
         den += rn * rn
         worst = max(worst, e / max(rn, 1e-30))
-    print(f"tp={g} {preset}: worst per-block grad rel-Frob {worst:.3e}, pooled {(num / den) ** 0.5:.3e}")
+    print(f"tp={g} sp={sp} {preset}: worst per-block grad rel-Frob {worst:.3e}, pooled {(num / den) ** 0.5:.3e}")
     assert worst <= 3e-2
     assert (num / den) ** 0.5 <= 2e-2
 
@@ -116,8 +121,8 @@ def test_tp_shards_are_slices_of_unsharded_model():
 
 
 def test_abi_nccl_comm_single_rank():
-    """The C-ABI TP collective (plora_tp_comm_init / plora_tp_allreduce over NCCL) on a
-    one-rank group: sum and max are the identity, bf16 and f32, on the current stream."""
+    """The C-ABI TP collectives (plora_tp_comm_init / allreduce / allgather / reducescatter /
+    reduce over NCCL) on a one-rank group: all are the identity, bf16 and f32."""
     from paper_2508_02932_b200.tp import AbiNcclComm
     comm = AbiNcclComm()
     try:
@@ -126,7 +131,12 @@ def test_abi_nccl_comm_single_rank():
             y = x.clone()
             comm.all_reduce_(y)
             comm.all_reduce_(y, "max")
+            comm.reduce_(y, 0)
+            g = torch.empty_like(y)
+            comm.all_gather_(g, y)
+            r = torch.empty_like(y)
+            comm.reduce_scatter_(r, g)
             torch.cuda.synchronize()
-            assert torch.equal(x, y)
+            assert torch.equal(x, y) and torch.equal(x, g) and torch.equal(x, r)
     finally:
         comm.close()

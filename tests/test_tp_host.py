@@ -118,3 +118,35 @@ def test_tp_sharding_and_collectives_gloo():
         assert e["row_fwd"] < 1e-12
         assert e["col_dA"] < 1e-9 and e["col_dX"] < 1e-9 and e["col_dB"] < 1e-12
         assert e["max"] == [1.0, 0.0]
+
+
+def _coll_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = DistComm()
+    x = torch.arange(6, dtype=torch.float32).reshape(3, 2) + 10 * rank
+    g = torch.empty(3 * world, 2)
+    comm.all_gather_(g, x)
+    full = torch.arange(4 * world, dtype=torch.float32).reshape(2 * world, 2) * (rank + 1)
+    rs = torch.empty(2, 2)
+    comm.reduce_scatter_(rs, full)
+    t = torch.full((3,), float(rank + 1))
+    comm.reduce_(t, 1)
+    out[rank] = (g.tolist(), rs.tolist(), t.tolist())
+    dist.destroy_process_group()
+
+
+def test_sequence_parallel_collectives_gloo():
+    """all_gather_ / reduce_scatter_ / reduce_ semantics of the TP communicator (the
+    sequence-parallel pieces) under gloo, world size 2."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_coll_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    base = torch.arange(6, dtype=torch.float32).reshape(3, 2)
+    want_g = torch.cat([base, base + 10]).tolist()
+    full = torch.arange(8, dtype=torch.float32).reshape(4, 2)
+    for r in range(2):
+        g, rs, t = out[r]
+        assert g == want_g
+        assert rs == (full * 3)[2 * r:2 * r + 2].tolist()     # (rank 0 x1 + rank 1 x2) rows of this rank
+    assert out[1][2] == [3.0, 3.0, 3.0]                        # reduce onto rank 1

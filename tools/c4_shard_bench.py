@@ -1,9 +1,9 @@
 """C4 (Qwen2.5-32B, 32 packed adapters, TP = 8) on ONE B200: times one tensor-parallel
-rank's shard of the step with the collectives replaced by no-ops.  The full 64-layer
-shard does not fit one 180 GB B200 at T = 32,768 (replicated
-column-parallel A state + unsharded activations; sequence parallelism is the fix), so
-the shard is timed at two reduced depths and extrapolated linearly in the layer count
-(every layer is identical work; the lm_head / embedding / optimizer rest is the intercept).
+rank's shard of the step with the collectives replaced by local copies (sequence
+parallelism on: the rank's token shard of the residual stream, full-T column/row GEMMs).
+The shard is timed at two depths (default 32 and the full 64 layers) and the per-layer
+time is their slope (every layer is identical work; lm_head / embedding / optimizer are
+the intercept).
 
 This is a COMPUTE-ONLY projection (the pool has one GPU, so the NCCL all-reduces of
 a real TP=8 job cannot run here): every GEMM / LoRA / attention / optimizer kernel of
@@ -35,6 +35,17 @@ class NullComm(Comm):
     def all_reduce_(self, t, op="sum"):
         return t
 
+    def all_gather_(self, out, inp):
+        out[self.rank * inp.shape[0]:(self.rank + 1) * inp.shape[0]].copy_(inp)   # own rows; others stale
+        return out
+
+    def reduce_scatter_(self, out, inp):
+        out.copy_(inp[self.rank * out.shape[0]:(self.rank + 1) * out.shape[0]])
+        return out
+
+    def reduce_(self, t, root):
+        return t
+
 
 def time_shard(cfg, specs, s, tp, steps, warmup):
     tr = PackedLoraTrainer(cfg, specs, s, device="cuda", tp=NullComm(0, tp))
@@ -60,7 +71,7 @@ def main():
     ap.add_argument("--tp", type=int, default=8)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--depths", default="16,32")
+    ap.add_argument("--depths", default="32,64")
     args = ap.parse_args()
     full = PRESETS["qwen2.5-32b"]
     specs, s = bench_adapters("qwen2.5-32b")
