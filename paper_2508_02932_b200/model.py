@@ -214,7 +214,10 @@ class PackedLoraTrainer:
                  save_normed: bool | None = None, sequence_parallel: bool = True):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
-        the step inserts the all-reduces described in tp.py."""
+        the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
+        when tp divides T) also shards the residual stream over tokens.
+        ``save_normed``: keep the normed layer inputs for the backward (None: when the
+        activation estimate leaves headroom on the device)."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -288,16 +291,17 @@ class PackedLoraTrainer:
 
     def _row_fwd(self, layer: int, tname: str, x: torch.Tensor, w: torch.Tensor):
         """Row-parallel target (o, down).  Under TP the output Y_s = X_s W_s^T + Hs_s B^T is a
-        partial sum: its all-reduce runs per token chunk on a side stream, overlapping the
-        next chunk's GEMM; the partial Hs is all-reduced after the last chunk read it."""
+        partial sum reduced per token chunk on a side stream, overlapping the next chunk's
+        GEMM (see _overlapped; with sequence parallelism the rank's token shard is
+        returned); the partial Hs is all-reduced after the last chunk read it."""
         if self.tp is None:
             return self._lin_fwd(layer, tname, x, w)
         bank, meta = self.bank, self.meta
         hs = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
         ops.shrink(meta, x, bank.shadow_of(layer, tname, "A"), hs)
-        y = torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device)
+        y_part = torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device)
         bt = bank.shadow_of(layer, tname, "B")
-        y = self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y), y, extra=(hs,))
+        y = self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y_part), y_part, extra=(hs,))
         return y, hs
 
     def _overlapped(self, launch, y: torch.Tensor, extra=()):
@@ -393,9 +397,10 @@ class PackedLoraTrainer:
         dx = None
         ws, ashs = [lw[nm] for nm in names], [bank.shadow_of(layer, nm, "A") for nm in names]
         if need_dx and self.tp is not None:   # partial dX_s: chunked all-reduce overlapping the GEMM
-            dx = torch.empty((self.T, x.shape[1]), dtype=bf16, device=self.device)
-            dx = self._overlapped(lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx),
-                                  dx, extra=dhs)
+            dx_part = torch.empty((self.T, x.shape[1]), dtype=bf16, device=self.device)
+            dx = self._overlapped(
+                lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx_part),
+                dx_part, extra=dhs)
         else:
             if need_dx:   # K6 (Case 4) for every target in one accumulator
                 dx = ops.linear_dx_group(meta, list(dys), ws, ashs, dhs, x.shape[1])

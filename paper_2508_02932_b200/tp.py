@@ -18,6 +18,12 @@ PyTorch DTensor.  Here the packed trainer itself shards:
   lm_head: vocabulary-parallel with a two-pass cross entropy
       (``plora_ce_stats`` / ``plora_ce_apply``).
 
+Sequence parallelism (default when tp divides T): the residual stream and norms
+hold only the rank's T/tp token rows; the normed input is all-gathered before the
+column-parallel projections and the row-parallel partial outputs are reduced onto
+their owning rank (reduce-scatter), in the backward mirrored -- the same bytes as
+the all-reduce formulation with 1/tp of the activation memory.
+
 Replicated LoRA factors (column A, row B) get bit-identical gradients on every
 rank (identical inputs + deterministic kernels + all-reduced dH / Hs), so their
 AdamW states evolve identically without a gradient all-reduce.
