@@ -211,6 +211,9 @@ def main() -> None:
     tp = args.tp or (world if args.config == "qwen2.5-32b" else 1)
     if world % tp:
         raise SystemExit(f"--tp {tp} must divide the world size {world}")
+    if args.config == "qwen2.5-32b" and tp < 8:
+        raise SystemExit("C4 (Qwen2.5-32B, 32 adapters) needs a tensor-parallel group of 8 GPUs "
+                         "(one 180 GB B200 holds a TP=8 shard: tools/c4_shard_bench.py)")
     n_jobs = world // tp
     job = rank // tp
     comm = None
