@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 4
+#define PLORA_ABI_VERSION 5
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -150,7 +150,10 @@ PLORA_API int plora_linear_expand(void* stream, const plora_pack_t* pack,
 PLORA_API int plora_linear_expand_group(void* stream, const plora_pack_t* pack,
                      const void* X, int64_t d, int32_t n, const int64_t* k_out,
                      const void* const* W, int32_t w_kmajor, const void* const* Bt_sh,
-                     const void* const* Hs, void* const* Y);
+                     const void* const* Hs, void* const* Y,
+                     const void* const* bias /* may be NULL; bias[j] bf16 [k_out[j]] or NULL */);
+/* y[r][c] += bias[c] (bf16, rows x n, row pitch ldy). */
+PLORA_API int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias);
 
 /* gate/up projections fused with the SwiGLU forward: one pair-GEMM launch whose tiles
  * hold 256 gate and the same 256 up columns, so the epilogue writes

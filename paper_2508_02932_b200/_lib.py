@@ -31,6 +31,7 @@ EXPORTS = (
     "plora_lora_segred_multi",
     "plora_linear_expand",
     "plora_linear_expand_group",
+    "plora_add_row_bias",
     "plora_linear_dx_group",
     "plora_linear_gate_up_swiglu",
     "plora_linear_bwd",
@@ -53,7 +54,7 @@ EXPORTS = (
     "plora_tp_reduce",
 )
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class PloraError(RuntimeError):
@@ -110,7 +111,9 @@ _SIGNATURES = {
     "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                              _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_expand_group": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i32, _p64, ctypes.POINTER(_vp),
-                                   _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)], ctypes.c_int),
+                                   _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                   ctypes.POINTER(_vp)], ctypes.c_int),
+    "plora_add_row_bias": ([_vp, _i64, _i64, _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_dx_group": ([_vp, ctypes.POINTER(PackStruct), _i32, ctypes.POINTER(_vp), _p64, ctypes.POINTER(_vp),
                                _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_gate_up_swiglu": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64] + [_vp] * 9, ctypes.c_int),

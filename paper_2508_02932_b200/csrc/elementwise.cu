@@ -414,6 +414,21 @@ __global__ void ce_apply_kernel(bf16* __restrict__ logits, const int64_t* __rest
   }
 }
 
+// y[r][c] = bf16(float(y[r][c]) + float(bias[c])) -- a broadcast row bias (narrow q/k/v shards).
+__global__ void add_row_bias_kernel(bf16* __restrict__ y, const bf16* __restrict__ bias, int64_t rows, int64_t n,
+                                    int64_t ldy) {
+  const int64_t per = n / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * per; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per, c = (i - r * per) * 8;
+    float f[8], b[8];
+    load8(y + r * ldy + c, f);
+    load8(bias + c, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] += b[e];
+    store8(y + r * ldy + c, f);
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -500,6 +515,14 @@ PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* l
   ce_kernel<<<rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<bf16*>(logits), labels, weight, tok_loss, (int)V);
   return launch_status("cross_entropy");
+}
+
+PLORA_API int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias) {
+  if (rows <= 0 || n <= 0) return 0;
+  if (n % 8 || ldy % 8) return plora::set_error("add_row_bias: n and ldy must be multiples of 8");
+  add_row_bias_kernel<<<grid_for(rows * (n / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<bf16*>(y), static_cast<const bf16*>(bias), rows, n, ldy);
+  return launch_status("add_row_bias");
 }
 
 PLORA_API int plora_ce_stats(void* stream, int64_t rows, int64_t V, const void* logits, const int64_t* labels,

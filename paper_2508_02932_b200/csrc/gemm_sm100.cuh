@@ -496,6 +496,7 @@ struct __align__(64) PairArgs {
   int32_t paired;          // gate/up + SwiGLU: chunk c of every 256-column tile is segment c (see EPI_SWIGLU)
   void* seg_out[3];        // N-segments: output base (masked direct stores)
   int64_t seg_ldo[3];
+  const void* seg_bias[3]; // N-segments: optional bf16 bias [N] added in the epilogue
 };
 
 // Epilogue variants of the pair kernel.
@@ -581,7 +582,19 @@ struct PairOut {
   int64_t ldo;
   int N;
   int accumulate;
+  const __nv_bfloat16* bias;   // optional per-column bias (q/k/v of Qwen2), added to the bf16 result
 };
+
+// Word q (columns col0 + 2q, +1) of a bf16-packed chunk, plus the optional bias with the
+// rounding of adding a bf16 bias to the bf16 output: round(float(y) + float(b)).
+__device__ __forceinline__ uint32_t chunk_word(const PairOut& po, int col0, const uint32_t (&v)[16], int q) {
+  if (po.bias == nullptr) return v[q];
+  const int c = col0 + 2 * q;
+  const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[q]));
+  const float b0 = c < po.N ? __bfloat162float(po.bias[c]) : 0.f;
+  const float b1 = c + 1 < po.N ? __bfloat162float(po.bias[c + 1]) : 0.f;
+  return pack_bf16x2(y.x + b0, y.y + b1);
+}
 
 __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg, int& issued, int lane, int col0,
                                                 int m0, int m_len, const uint32_t (&v)[16]) {
@@ -595,7 +608,8 @@ __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg,
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       *reinterpret_cast<uint4*>(buf + lane * 64 + 16 * (q ^ ((lane >> 1) & 3))) =
-          make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          make_uint4(chunk_word(po, col0, v, 4 * q), chunk_word(po, col0, v, 4 * q + 1),
+                     chunk_word(po, col0, v, 4 * q + 2), chunk_word(po, col0, v, 4 * q + 3));
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -606,12 +620,12 @@ __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg,
     ++issued;
   } else if (lane < m_len) {
     __nv_bfloat16* o = po.out + static_cast<int64_t>(m0 + lane) * po.ldo;
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int cc = col0 + 2 * q;
       if (cc < po.N) {
-        float2 f = __bfloat1622float2(h[q]);
+        const uint32_t w = chunk_word(po, col0, v, q);
+        float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
         if (po.accumulate) {
           const float2 old = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + cc));
           f.x += old.x;
@@ -841,6 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
         pg.ldo = pu.ldo = pa.ldo = p.seg_ldo[0];
         pg.N = pu.N = pa.N = p.seg_N[0];
         pg.accumulate = pu.accumulate = pa.accumulate = 0;
+        pg.bias = pu.bias = pa.bias = nullptr;
         uint32_t kg[kPairs - kDirectPairs][16], ku[kPairs - kDirectPairs][16];
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
@@ -890,6 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       po.ldo = p.seg_ldo[t.seg];
       po.N = p.seg_N[t.seg];
       po.accumulate = args.accumulate;
+      po.bias = static_cast<const __nv_bfloat16*>(p.seg_bias[t.seg]);
       uint32_t pk[kParked > 0 ? kParked : 1][16];
       if (!skip) {
         uint32_t r[32];

@@ -206,6 +206,7 @@ struct PairSeg {
   const void* L;   // LoRA B operand [n][N][64nb]
   void* Y;         // [M][ldy] (K-segments: segment 0's is the shared output)
   int64_t ldy;
+  const void* bias = nullptr;   // optional bf16 [N] added to the bf16 result (N-segments)
 };
 
 // CTA-pair GEMM over 1..3 N-segments (shared A) or K-segments (shared output).
@@ -256,6 +257,7 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
       if ((rc = make_map_out(mY[s], g.Y, N, M, g.ldy))) return rc;
       pa.seg_out[s] = g.Y;
       pa.seg_ldo[s] = g.ldy;
+      pa.seg_bias[s] = g.bias;
       pa.seg_N[s] = static_cast<int>(N);
       if (!paired || s == 0) nt += static_cast<int>((N + (paired ? 256 : tile_n) - 1) / (paired ? 256 : tile_n));
       pa.seg_nt_end[s] = nt;
@@ -649,9 +651,12 @@ static bool group_pair_ok(const plora_pack_t* pack, int n, const int64_t* N) {
   return true;
 }
 
+int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias);
+
 int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int32_t n,
                               const int64_t* k_out, const void* const* W, int32_t w_kmajor,
-                              const void* const* Bt_sh, const void* const* Hs, void* const* Y) {
+                              const void* const* Bt_sh, const void* const* Hs, void* const* Y,
+                              const void* const* bias) {
   int rc;
   if ((rc = check_pack(pack))) return rc;
   if (n < 1 || n > 3) return fail("expand_group: 1..3 targets");
@@ -659,13 +664,16 @@ int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void
   const int64_t T = pack->total_tokens;
   if (T <= 0) return 0;
   if (!group_pair_ok(pack, n, k_out)) {   // narrow targets: one launch per target
-    for (int j = 0; j < n; ++j)
+    for (int j = 0; j < n; ++j) {
       if ((rc = run_gemm(st, pack, T, k_out[j], d, X, W[j], w_kmajor, Hs[j], Bt_sh[j], Y[j], k_out[j], nullptr)))
         return rc;
+      if (bias && bias[j] && (rc = plora_add_row_bias(stream, T, k_out[j], Y[j], k_out[j], bias[j]))) return rc;
+    }
     return 0;
   }
   PairSeg sg[3];
-  for (int j = 0; j < n; ++j) sg[j] = PairSeg{X, d, W[j], k_out[j], Hs[j], Bt_sh[j], Y[j], k_out[j]};
+  for (int j = 0; j < n; ++j)
+    sg[j] = PairSeg{X, d, W[j], k_out[j], Hs[j], Bt_sh[j], Y[j], k_out[j], bias ? bias[j] : nullptr};
   return run_pair_segments(st, pack, T, n, 1, sg, w_kmajor, nullptr);
 }
 

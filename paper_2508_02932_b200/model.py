@@ -371,14 +371,14 @@ class PackedLoraTrainer:
                               bank.region_flat(bank.G, layer, tname, "B"),
                               dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
 
-    def _group_fwd(self, layer: int, names, x: torch.Tensor):
+    def _group_fwd(self, layer: int, names, x: torch.Tensor, biases=None):
         """Forward of targets sharing the input x (q/k/v or gate/up): ONE K2a launch reads
         x once for every target's Hs, then ONE grouped K1 GEMM (K2b fused) for all targets."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
         hss = [torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device) for _ in names]
         ops.shrink_multi(meta, x, [bank.shadow_of(layer, nm, "A") for nm in names], hss)
         ys = ops.linear_expand_group(meta, x, [lw[nm] for nm in names],
-                                     [bank.shadow_of(layer, nm, "B") for nm in names], hss)
+                                     [bank.shadow_of(layer, nm, "B") for nm in names], hss, biases=biases)
         return ys, hss
 
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
@@ -437,13 +437,10 @@ class PackedLoraTrainer:
         else:
             h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
         x1 = self._gather(x1)     # sequence parallel: the rank's token shard -> all T rows
-        (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1)
+        biases = [lw["q_bias"], lw["k_bias"], lw["v_bias"]] if cfg.qkv_bias else None   # added in the epilogue
+        (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1, biases)
         x1_keep = x1 if self.save_normed else None
         del x1
-        if cfg.qkv_bias:
-            q += lw["q_bias"]
-            k += lw["k_bias"]
-            v += lw["v_bias"]
         ew.rope(q.view(B, s, H, hd), self.cos, self.sin, s, out=q)        # in place
         ew.rope(k.view(B, s, KV, hd), self.cos, self.sin, s, out=k)
         qg = q.view(B, s, H, hd).transpose(1, 2).detach().requires_grad_()

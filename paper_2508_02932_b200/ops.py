@@ -198,9 +198,10 @@ def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
     return gs
 
 
-def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmajor: bool = True) -> list:
+def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmajor: bool = True,
+                        biases=None) -> list:
     """K1 + K2b for targets sharing x (q/k/v, gate/up) in ONE pair-GEMM launch:
-    y_j = x op(W_j) + Hs_j,i B_j,i (returns the new y_j [T][k_j])."""
+    y_j = x op(W_j) + Hs_j,i B_j,i (+ bias_j, in the epilogue) (returns the new y_j [T][k_j])."""
     T, d = x.shape
     ks = [w.shape[0] if w_kmajor else w.shape[1] for w in ws]
     ys = [torch.empty((T, k), dtype=torch.bfloat16, device=x.device) for k in ks]
@@ -210,8 +211,15 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
     bp, _k2 = _ptr_array(bt_shs, "bt_sh")
     hp, _k3 = _ptr_array(hss, "hs")
     yp, _k4 = _ptr_array(ys, "y")
+    if biases is not None:
+        barr = (ctypes.c_void_p * len(ws))(*[None if b is None else _need(b, f"bias[{j}]") for j, b in
+                                             enumerate(biases)])
+        bip = ctypes.cast(barr, ctypes.POINTER(ctypes.c_void_p))
+    else:
+        bip = None
     _lib.check(_lib.lib().plora_linear_expand_group(_stream(), ctypes.byref(meta.struct), _need(x, "x"), d, len(ws),
-                                                    karr, wp, int(w_kmajor), bp, hp, yp), "plora_linear_expand_group")
+                                                    karr, wp, int(w_kmajor), bp, hp, yp, bip),
+               "plora_linear_expand_group")
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)

@@ -261,3 +261,23 @@ def test_gate_up_swiglu_fused_matches_unfused(ffn):
     torch.cuda.synchronize()
     assert torch.equal(g, rg) and torch.equal(u, ru)
     assert torch.equal(act, ew.swiglu_fwd(rg, ru))
+
+
+@pytest.mark.parametrize("widths", [[1024, 256, 512], [512, 128, 128]])
+def test_grouped_expand_bias_epilogue(widths):
+    """q/k/v biases added in the grouped GEMM epilogue (or by plora_add_row_bias when a
+    narrow target forces separate launches) == the bf16 output + bf16 bias, bit for bit."""
+    ranks, tokens = [8, 64, 16], [1024, 333, 700]
+    d = 512
+    meta = build_meta(ranks, tokens, [2.0 * r for r in ranks]).to("cuda")
+    T, R64, n = meta.total_tokens, meta.rpad64, len(ranks)
+    g = torch.Generator(device="cuda").manual_seed(41)
+    x = torch.randn(T, d, device="cuda", generator=g).to(bf)
+    ws = [(torch.randn(k, d, device="cuda", generator=g) * 0.05).to(bf) for k in widths]
+    bts = [(torch.randn(n, k, R64, device="cuda", generator=g) * 0.05).to(bf) for k in widths]
+    hss = [torch.randn(T, R64, device="cuda", generator=g).to(bf) for _ in widths]
+    bs = [torch.randn(k, device="cuda", generator=g).to(bf) for k in widths]
+    ys = ops.linear_expand_group(meta, x, ws, bts, hss, biases=bs)
+    refs = ops.linear_expand_group(meta, x, ws, bts, hss)
+    for y, r, b in zip(ys, refs, bs):
+        assert torch.equal(y, r + b)
