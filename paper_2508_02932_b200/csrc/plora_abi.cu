@@ -181,6 +181,11 @@ static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   return 0;
 }
 
+static int g_pair_nb1_max_k = [] {   // K at or below which 256x256 double-buffered tiles are used
+  const char* e = getenv("PLORA_PAIR_NB1_MAXK");
+  return e ? atoi(e) : 1024;   // C4 TP shards (o: K = 640, q/k/v dX: K = 896): ~1% per layer
+}();
+
 static int g_pair_nb_min_n = [] {   // N at which the 256x512 pair tile is used
   const char* e = getenv("PLORA_PAIR512_MIN_N");
   return e ? atoi(e) : 2048;
@@ -222,7 +227,12 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
   const bool paired = swiglu_act != nullptr;   // gate/up + SwiGLU (EPI_SWIGLU): segments 0, 1 share columns
   if (paired && (n_seg != 2 || sg[0].N != sg[1].N || !w_kmajor || residual))
     return fail("gate/up SwiGLU GEMM: two equal-width nn.Linear-layout segments");
-  const int NB = paired ? 2 : ((n_seg > 1 ? Ntot : Nmin) >= g_pair_nb_min_n ? 2 : 1);
+  int64_t Ktot = 0;
+  for (int s = 0; s < (k_seg > 1 ? k_seg : 1); ++s) Ktot += sg[s].K;
+  // 256 x 512 tiles (single accumulator) unless the output is narrow or the K loop is so
+  // short that the epilogue bubble outweighs the operand-traffic saving (then 256 x 256
+  // tiles with a double-buffered accumulator)
+  const int NB = paired ? 2 : (((n_seg > 1 ? Ntot : Nmin) >= g_pair_nb_min_n && Ktot > g_pair_nb1_max_k) ? 2 : 1);
   const int tile_n = 256 * NB;
   PairArgs pa;
   memset(&pa, 0, sizeof(pa));
