@@ -654,11 +654,19 @@ int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, i
                   Hs, Bt_sh, Y, ldy, residual);
 }
 
+static int g_group_min_n = [] {   // narrowest grouped segment (narrower: separate launches)
+  const char* e = getenv("PLORA_GROUP_MIN_N");
+  return e ? atoi(e) : 64;   // narrow TP-shard k/v (N = 128) ride the grouped launch: ~1% per C4 layer
+}();
+
 static bool group_pair_ok(const plora_pack_t* pack, int n, const int64_t* N) {
   if (!g_pair_enabled || (pack->d_ptiles == nullptr && pack->n_ptiles != 0)) return false;
-  for (int j = 0; j < n; ++j)
-    if (N[j] < 256) return false;
-  return true;
+  int64_t widest = 0;
+  for (int j = 0; j < n; ++j) {
+    if (N[j] < g_group_min_n) return false;
+    widest = N[j] > widest ? N[j] : widest;
+  }
+  return widest >= 256;
 }
 
 int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias);
