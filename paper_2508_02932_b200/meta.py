@@ -120,6 +120,28 @@ class PackMeta:
         self._dev[key] = out
         return out
 
+    def shard_launches(self, world: int, launches: int):
+        """Sequence-parallel shards grouped into <= `launches` pair-GEMM launches:
+        [(sub_meta, [(owner, row_lo, row_hi), ...])] -- each launch covers consecutive
+        whole shards (fewer, fuller launches than one per shard), or None when the
+        shards cannot be cut at pair-tile boundaries."""
+        key = ("shard_launches", world, launches)
+        if key in self._dev:
+            return self._dev[key]
+        per = self.shard_tile_chunks(world)
+        out = None
+        if per is not None:
+            groups = max(1, min(launches, world))
+            bounds = [round(i * world / groups) for i in range(groups + 1)]
+            out = []
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                if b <= a:
+                    continue
+                lo, hi = self._shard_tiles[world][a][0], self._shard_tiles[world][b - 1][1]
+                out.append((self._sub(lo, hi), [(r, per[r][1], per[r][2]) for r in range(a, b)]))
+        self._dev[key] = out
+        return out
+
     def shard_tile_chunks(self, world: int):
         """The pair-tile list cut exactly at the sequence-parallel shard boundaries
         (rows r * T / world): [(sub_meta, row_lo, row_hi)] per shard, or None when a
@@ -140,6 +162,9 @@ class PackMeta:
                 cuts.append(int(j[0]))
             if cuts is not None:
                 cuts.append(self.ptiles.shape[0])
+                if not hasattr(self, "_shard_tiles"):
+                    self._shard_tiles = {}
+                self._shard_tiles[world] = list(zip(cuts[:-1], cuts[1:]))
                 out = [(self._sub(lo, hi), r * (T // world), (r + 1) * (T // world))
                        for r, (lo, hi) in enumerate(zip(cuts[:-1], cuts[1:]))]
         self._dev[key] = out

@@ -320,7 +320,7 @@ class PackedLoraTrainer:
         wide = y.shape[1] >= 256   # pair-GEMM path (sub-packs only restrict pair tiles)
         out = y
         if self.sp:
-            chunks = self.meta.shard_tile_chunks(self.shard.world) if wide else None
+            chunks = self.meta.shard_launches(self.shard.world, self.tp_chunks) if wide else None
             if chunks is None:
                 launch(self.meta)
                 out = torch.empty((self.Tl, y.shape[1]), dtype=y.dtype, device=y.device)
@@ -329,14 +329,15 @@ class PackedLoraTrainer:
                 side.wait_event(ev)
                 with torch.cuda.stream(side):
                     self.tp.reduce_scatter_(out, y)
-            else:
-                for owner, (sub, r0, r1) in enumerate(chunks):
+            else:   # launches of whole shards; each shard reduced onto its owner after its launch
+                for sub, shards in chunks:
                     launch(sub)
                     ev = torch.cuda.Event()
                     ev.record(cur)
                     side.wait_event(ev)
                     with torch.cuda.stream(side):
-                        self.tp.reduce_(y[r0:r1], owner)
+                        for owner, r0, r1 in shards:
+                            self.tp.reduce_(y[r0:r1], owner)
                 out = y[self.r0:self.r0 + self.Tl]
         else:
             chunks = self.meta.tile_chunks(self.tp_chunks) if wide else [(self.meta, 0, self.T)]
