@@ -356,6 +356,29 @@ class PackedLoraTrainer:
         cur.wait_event(done)
         return out
 
+    def _prefetch_normed(self, h, rstd, w):
+        """Recompute rmsnorm(h) and (sequence parallel) all-gather it -- on the side stream
+        when TP is active, so it overlaps the compute issued meanwhile; _await joins it."""
+        if not self.sp:
+            return ("ready", ew.rmsnorm_apply(h, rstd, w))
+        cur = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            x = self._gather(ew.rmsnorm_apply(h, rstd, w))
+            ev = torch.cuda.Event()
+            ev.record(side)
+        x.record_stream(cur)   # consumed on the compute stream
+        return ("pending", x, ev)
+
+    def _await(self, pre):
+        if pre[0] == "ready":
+            return pre[1]
+        torch.cuda.current_stream().wait_event(pre[2])
+        return pre[1]
+
     def _gather(self, x_s: torch.Tensor) -> torch.Tensor:
         """Sequence parallelism: every rank's [T/tp][d] token shard -> the full [T][d]."""
         if not self.sp:
@@ -483,6 +506,10 @@ class PackedLoraTrainer:
         # Cases 2/1/4 run first; the SwiGLU backward re-emits the activation in the same
         # pass (no separate recompute), then Case 3 dA_down = act^T dH.
         bank, meta = self.bank, self.meta
+        # sequence parallel, normed inputs not kept: start re-gathering x2 and x1 on the side
+        # stream now, so the all-gathers overlap the down / o projection backward below
+        pre2 = self._prefetch_normed(sv.h_mid, sv.rstd2, lw["mlp_norm"]) if sv.x2 is None else None
+        pre1 = self._prefetch_normed(sv.h_in, sv.rstd1, lw["attn_norm"]) if sv.x1 is None else None
         dh_s = dh
         dh = self._gather(dh_s)   # sequence parallel: the row-parallel output gradient on all T rows
         dh_down = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
@@ -495,7 +522,7 @@ class PackedLoraTrainer:
         del d_act
         ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
         del act, dh_down
-        x2 = sv.x2 if sv.x2 is not None else self._gather(ew.rmsnorm_apply(sv.h_mid, sv.rstd2, lw["mlp_norm"]))
+        x2 = sv.x2 if sv.x2 is not None else self._await(pre2)
         sv.x2 = None
         dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))
         del dg, du, x2
@@ -508,7 +535,7 @@ class PackedLoraTrainer:
         dq = ew.rope(dq.transpose(1, 2), self.cos, self.sin, s, inverse=True)      # [T][H*hd]
         dk = ew.rope(dk.transpose(1, 2), self.cos, self.sin, s, inverse=True)
         dv = self._token_major(dv)
-        x1 = sv.x1 if sv.x1 is not None else self._gather(ew.rmsnorm_apply(sv.h_in, sv.rstd1, lw["attn_norm"]))
+        x1 = sv.x1 if sv.x1 is not None else self._await(pre1)
         sv.x1 = None
         dx1 = self._group_bwd(layer, ("v", "k", "q"), x1, (sv.hs["v"], sv.hs["k"], sv.hs["q"]), (dv, dk, dq),
                               need_dx=need_dx)

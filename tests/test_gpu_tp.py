@@ -19,11 +19,11 @@ from paper_2508_02932_b200.tp import TPShard, run_threaded
 pytestmark = pytest.mark.gpu
 
 
-def _make(preset, tp=None, sp=True):
+def _make(preset, tp=None, sp=True, save_normed=None):
     cfg = PRESETS[preset]
     specs, s = bench_adapters(preset)
     return PackedLoraTrainer(cfg, specs, s, device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in specs],
-                             tp=tp, sequence_parallel=sp)
+                             tp=tp, sequence_parallel=sp, save_normed=save_normed)
 
 
 def _grads(tr):
@@ -45,19 +45,21 @@ def _masters(tr):
             for i in range(tr.meta.n_adapters)}
 
 
-@pytest.mark.parametrize("preset,g,sp", [("tiny-qwen", 2, True), ("tiny", 4, True), ("tiny-qwen", 2, False),
-                                         ("tiny", 4, False)])
-def test_tp_matches_unsharded(preset, g, sp):
+@pytest.mark.parametrize("preset,g,sp,keep", [("tiny-qwen", 2, True, True), ("tiny", 4, True, True),
+                                              ("tiny-qwen", 2, True, False), ("tiny-qwen", 2, False, True),
+                                              ("tiny", 4, False, True)])
+def test_tp_matches_unsharded(preset, g, sp, keep):
     """sp: Megatron sequence parallelism (token-sharded residual stream; g = 2 cuts the
     pair-tile list exactly at the shard boundaries -> per-shard reduces overlapping the
-    GEMM; g = 4 does not -> one reduce-scatter); sp = False: all-reduce chunks."""
+    GEMM; g = 4 does not -> one reduce-scatter); sp = False: all-reduce chunks.
+    keep = False: the normed inputs are re-gathered in the backward on the side stream."""
     ref = _make(preset)
     tokens = ref.synthetic_tokens().cuda()
     ref_losses = ref.forward_backward(tokens).double().cpu()
     ref_grads = _grads(ref)
 
     def rank_fn(comm):
-        tr = _make(preset, tp=comm, sp=sp)
+        tr = _make(preset, tp=comm, sp=sp, save_normed=keep)
         assert tr.sp == sp
         losses = tr.forward_backward(tokens).double().cpu()
         grads = _grads(tr)
