@@ -152,7 +152,7 @@ PLORA_API int plora_linear_expand_group(void* stream, const plora_pack_t* pack,
                      const void* const* W, int32_t w_kmajor, const void* const* Bt_sh,
                      const void* const* Hs, void* const* Y,
                      const void* const* bias /* may be NULL; bias[j] bf16 [k_out[j]] or NULL */);
-/* y[r][c] += bias[c] (bf16, rows x n, row pitch ldy). */
+/* y[r][c] += bias[c] (bf16, rows x n, row pitch ldy): a standalone broadcast row bias. */
 PLORA_API int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias);
 
 /* gate/up projections fused with the SwiGLU forward: one pair-GEMM launch whose tiles
@@ -265,6 +265,8 @@ PLORA_API int plora_tp_allgather(void* stream, void* comm, const void* send, voi
 PLORA_API int plora_tp_reducescatter(void* stream, void* comm, const void* send, void* recv, int64_t recv_count,
                                      int32_t dtype);
 PLORA_API int plora_tp_reduce(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t root);
+/* buf on every rank = buf on root (in place). */
+PLORA_API int plora_tp_broadcast(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t root);
 
 #ifdef __cplusplus
 }

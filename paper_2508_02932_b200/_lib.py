@@ -52,6 +52,7 @@ EXPORTS = (
     "plora_tp_allgather",
     "plora_tp_reducescatter",
     "plora_tp_reduce",
+    "plora_tp_broadcast",
 )
 
 ABI_VERSION = 5
@@ -138,6 +139,7 @@ _SIGNATURES = {
     "plora_tp_allgather": ([_vp, _vp, _vp, _vp, _i64, _i32], ctypes.c_int),
     "plora_tp_reducescatter": ([_vp, _vp, _vp, _vp, _i64, _i32], ctypes.c_int),
     "plora_tp_reduce": ([_vp, _vp, _vp, _i64, _i32, _i32], ctypes.c_int),
+    "plora_tp_broadcast": ([_vp, _vp, _vp, _i64, _i32, _i32], ctypes.c_int),
 }
 
 

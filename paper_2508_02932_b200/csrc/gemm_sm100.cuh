@@ -58,6 +58,7 @@ struct __align__(64) GemmArgs {
   CUtensorMap tmB3;
   void* out2;
   void* out3;
+  const __nv_bfloat16* bias;   // GEMM: optional per-column bias added to the bf16 result
 };
 
 constexpr int kBM = 128;
@@ -381,6 +382,12 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * scale;
+            if (MODE == MODE_GEMM && args.bias != nullptr) {   // round(round(y) + b): as a bf16 bias add
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < args.N)
+                  v[j] = __bfloat162float(__float2bfloat16_rn(v[j])) + __bfloat162float(args.bias[col0 + j]);
+            }
             if (col0 + 32 <= args.N) {
               if (res) {
 #pragma unroll

@@ -315,22 +315,22 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
 // CTA-pair GEMM (N >= 256), one problem.
 static int run_gemm_pair(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
                          const void* A, const void* W, int w_kmajor, const void* H, const void* L,
-                         void* Y, int64_t ldy, const void* residual) {
-  PairSeg sg{A, K, W, N, H, L, Y, ldy};
+                         void* Y, int64_t ldy, const void* residual, const void* bias = nullptr) {
+  PairSeg sg{A, K, W, N, H, L, Y, ldy, bias};
   return run_pair_segments(st, pack, M, 1, 1, &sg, w_kmajor, residual);
 }
 
 // Base GEMM (+ fused LoRA expand).  A: [M][K] K-major.  W: see w_kmajor.
 static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_t N, int64_t K,
                     const void* A, const void* W, int w_kmajor, const void* H, const void* L,
-                    void* Y, int64_t ldy, const void* residual) {
+                    void* Y, int64_t ldy, const void* residual, const void* bias = nullptr) {
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0) return fail("gemm: K must be positive");
   if (K % 8 || N % 8 || ldy % 8) return fail("gemm: K, N and ldy must be multiples of 8");
   if (reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16))
     return fail("gemm: output/residual must be 16-byte aligned");
   if (g_pair_enabled && N >= 256 && (pack == nullptr || pack->d_ptiles != nullptr || pack->n_ptiles == 0))
-    return run_gemm_pair(st, pack, M, N, K, A, W, w_kmajor, H, L, Y, ldy, residual);
+    return run_gemm_pair(st, pack, M, N, K, A, W, w_kmajor, H, L, Y, ldy, residual, bias);
   const int BN = pick_bn(N);
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -357,6 +357,7 @@ static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_
   a.out = Y;
   a.ldo = ldy;
   a.residual = static_cast<const __nv_bfloat16*>(residual);
+  a.bias = static_cast<const __nv_bfloat16*>(bias);
   if (BN == 256) return w_kmajor ? launch<256, MODE_GEMM, false>(a, st) : launch<256, MODE_GEMM, true>(a, st);
   if (BN == 128) return w_kmajor ? launch<128, MODE_GEMM, false>(a, st) : launch<128, MODE_GEMM, true>(a, st);
   return w_kmajor ? launch<64, MODE_GEMM, false>(a, st) : launch<64, MODE_GEMM, true>(a, st);
@@ -669,8 +670,6 @@ static bool group_pair_ok(const plora_pack_t* pack, int n, const int64_t* N) {
   return widest >= 256;
 }
 
-int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias);
-
 int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void* X, int64_t d, int32_t n,
                               const int64_t* k_out, const void* const* W, int32_t w_kmajor,
                               const void* const* Bt_sh, const void* const* Hs, void* const* Y,
@@ -682,11 +681,10 @@ int plora_linear_expand_group(void* stream, const plora_pack_t* pack, const void
   const int64_t T = pack->total_tokens;
   if (T <= 0) return 0;
   if (!group_pair_ok(pack, n, k_out)) {   // narrow targets: one launch per target
-    for (int j = 0; j < n; ++j) {
-      if ((rc = run_gemm(st, pack, T, k_out[j], d, X, W[j], w_kmajor, Hs[j], Bt_sh[j], Y[j], k_out[j], nullptr)))
+    for (int j = 0; j < n; ++j)
+      if ((rc = run_gemm(st, pack, T, k_out[j], d, X, W[j], w_kmajor, Hs[j], Bt_sh[j], Y[j], k_out[j], nullptr,
+                         bias ? bias[j] : nullptr)))
         return rc;
-      if (bias && bias[j] && (rc = plora_add_row_bias(stream, T, k_out[j], Y[j], k_out[j], bias[j]))) return rc;
-    }
     return 0;
   }
   PairSeg sg[3];

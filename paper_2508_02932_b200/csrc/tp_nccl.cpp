@@ -34,6 +34,7 @@ struct NcclApi {
                                  cudaStream_t) = nullptr;
   ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                          cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   bool ok = false;
 };
 
@@ -53,8 +54,9 @@ const NcclApi& api() {
     a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
     a.reduce_scatter = reinterpret_cast<decltype(a.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
     a.reduce = reinterpret_cast<decltype(a.reduce)>(dlsym(h, "ncclReduce"));
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(h, "ncclBroadcast"));
     a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_reduce && a.error_string &&
-           a.all_gather && a.reduce_scatter && a.reduce;
+           a.all_gather && a.reduce_scatter && a.reduce && a.broadcast;
   });
   return a;
 }
@@ -168,6 +170,18 @@ PLORA_API int plora_tp_reduce(void* stream, void* comm, void* buf, int64_t count
   const ncclResult_t r = a.reduce(buf, buf, static_cast<size_t>(count), dt, ncclSum, root,
                                   static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream));
   return r == ncclSuccess ? 0 : nccl_fail("ncclReduce", r);
+}
+
+PLORA_API int plora_tp_broadcast(void* stream, void* comm, void* buf, int64_t count, int32_t dtype, int32_t root) {
+  const NcclApi& a = api();
+  if (!a.ok) return plora::set_error("tp: libnccl.so.2 not available");
+  if (!comm) return plora::set_error("tp: comm is NULL");
+  if (count <= 0) return count == 0 ? 0 : plora::set_error("tp: negative count");
+  ncclDataType_t dt;
+  if (nccl_dtype(dtype, &dt)) return 1;
+  const ncclResult_t r = a.broadcast(buf, buf, static_cast<size_t>(count), dt, root, static_cast<ncclComm_t>(comm),
+                                     static_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? 0 : nccl_fail("ncclBroadcast", r);
 }
 
 }  // extern "C"

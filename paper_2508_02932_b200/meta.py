@@ -120,6 +120,14 @@ class PackMeta:
         self._dev[key] = out
         return out
 
+    def shard_launches_rows(self, world: int, launches: int):
+        """shard_launches whose sub-packs also restrict the 128-row tile list (so the
+        K2a shrinks of a launch cover exactly its rows), or None."""
+        out = self.shard_launches(world, launches)
+        if out is None or self._shard_mtiles.get(world) is None:
+            return None
+        return out
+
     def shard_launches(self, world: int, launches: int):
         """Sequence-parallel shards grouped into <= `launches` pair-GEMM launches:
         [(sub_meta, [(owner, row_lo, row_hi), ...])] -- each launch covers consecutive
@@ -134,11 +142,13 @@ class PackMeta:
             groups = max(1, min(launches, world))
             bounds = [round(i * world / groups) for i in range(groups + 1)]
             out = []
+            mt = self._shard_mtiles.get(world)
             for a, b in zip(bounds[:-1], bounds[1:]):
                 if b <= a:
                     continue
                 lo, hi = self._shard_tiles[world][a][0], self._shard_tiles[world][b - 1][1]
-                out.append((self._sub(lo, hi), [(r, per[r][1], per[r][2]) for r in range(a, b)]))
+                mlo, mhi = (mt[a][0], mt[b - 1][1]) if mt is not None else (None, None)
+                out.append((self._sub(lo, hi, mlo, mhi), [(r, per[r][1], per[r][2]) for r in range(a, b)]))
         self._dev[key] = out
         return out
 
@@ -165,13 +175,26 @@ class PackMeta:
                 if not hasattr(self, "_shard_tiles"):
                     self._shard_tiles = {}
                 self._shard_tiles[world] = list(zip(cuts[:-1], cuts[1:]))
+                mstarts = self.mtiles[:, 0].astype(np.int64)
+                mcuts = [0]
+                for r in range(1, world):
+                    j = np.flatnonzero(mstarts == r * (T // world))
+                    if j.size == 0:
+                        mcuts = None
+                        break
+                    mcuts.append(int(j[0]))
+                if not hasattr(self, "_shard_mtiles"):
+                    self._shard_mtiles = {}
+                self._shard_mtiles[world] = (None if mcuts is None else
+                                             list(zip(mcuts, mcuts[1:] + [self.mtiles.shape[0]])))
                 out = [(self._sub(lo, hi), r * (T // world), (r + 1) * (T // world))
                        for r, (lo, hi) in enumerate(zip(cuts[:-1], cuts[1:]))]
         self._dev[key] = out
         return out
 
-    def _sub(self, lo: int, hi: int) -> "PackMeta":
-        """This pack restricted to pair tiles [lo, hi) (pair-GEMM launches only)."""
+    def _sub(self, lo: int, hi: int, mlo: int | None = None, mhi: int | None = None) -> "PackMeta":
+        """This pack restricted to pair tiles [lo, hi) (pair-GEMM launches only) and, when
+        given, to 128-row tiles [mlo, mhi) (so K2a shrinks cover the same rows)."""
         import copy
 
         s = self.struct
@@ -180,6 +203,9 @@ class PackMeta:
         ctypes.pointer(st)[0] = s
         st.d_ptiles = s.d_ptiles + lo * 16
         st.n_ptiles = hi - lo
+        if mlo is not None:
+            st.d_mtiles = s.d_mtiles + mlo * 16
+            st.n_mtiles = mhi - mlo
         sub._struct = st
         sub._dev = self._dev
         if hasattr(sub, "_work"):

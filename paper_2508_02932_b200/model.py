@@ -395,15 +395,76 @@ class PackedLoraTrainer:
                               bank.region_flat(bank.G, layer, tname, "B"),
                               dx_out=dx_out, need_dx=need_dx, dx_residual=dx_residual)
 
-    def _group_fwd(self, layer: int, names, x: torch.Tensor, biases=None):
+    def _group_fwd(self, layer: int, names, x: torch.Tensor, biases=None, parts=None):
         """Forward of targets sharing the input x (q/k/v or gate/up): ONE K2a launch reads
-        x once for every target's Hs, then ONE grouped K1 GEMM (K2b fused) for all targets."""
+        x once for every target's Hs, then ONE grouped K1 GEMM (K2b fused) for all targets
+        -- per row part when x arrives in parts (sequence-parallel all-gather, see
+        _gather_parts: each part's kernels wait only for that part's rows)."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
         hss = [torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device) for _ in names]
-        ops.shrink_multi(meta, x, [bank.shadow_of(layer, nm, "A") for nm in names], hss)
-        ys = ops.linear_expand_group(meta, x, [lw[nm] for nm in names],
-                                     [bank.shadow_of(layer, nm, "B") for nm in names], hss, biases=biases)
+        a_shs = [bank.shadow_of(layer, nm, "A") for nm in names]
+        bt_shs = [bank.shadow_of(layer, nm, "B") for nm in names]
+        ws = [lw[nm] for nm in names]
+        if parts is None:
+            ops.shrink_multi(meta, x, a_shs, hss)
+            return ops.linear_expand_group(meta, x, ws, bt_shs, hss, biases=biases), hss
+        ys = [torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device) for w in ws]
+        cur = torch.cuda.current_stream()
+        for sub, ev in parts:
+            cur.wait_event(ev)
+            ops.shrink_multi(sub, x, a_shs, hss)
+            ops.linear_expand_group(sub, x, ws, bt_shs, hss, biases=biases, y_outs=ys)
         return ys, hss
+
+    def _gate_up_swiglu(self, layer: int, x: torch.Tensor, parts=None):
+        """gate/up with the SwiGLU forward in the GEMM epilogue (per row part, as _group_fwd)."""
+        bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
+        hs_g = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
+        hs_u = torch.empty_like(hs_g)
+        a_shs = [bank.shadow_of(layer, "gate", "A"), bank.shadow_of(layer, "up", "A")]
+        bts = (bank.shadow_of(layer, "gate", "B"), bank.shadow_of(layer, "up", "B"))
+        if parts is None:
+            ops.shrink_multi(meta, x, a_shs, [hs_g, hs_u])
+            g, u, act = ops.linear_gate_up_swiglu(meta, x, lw["gate"], lw["up"], *bts, hs_g, hs_u)
+            return g, u, act, hs_g, hs_u
+        ffn = lw["gate"].shape[0]
+        outs = tuple(torch.empty((self.T, ffn), dtype=bf16, device=self.device) for _ in range(3))
+        cur = torch.cuda.current_stream()
+        for sub, ev in parts:
+            cur.wait_event(ev)
+            ops.shrink_multi(sub, x, a_shs, [hs_g, hs_u])
+            ops.linear_gate_up_swiglu(sub, x, lw["gate"], lw["up"], *bts, hs_g, hs_u, outs=outs)
+        return (*outs, hs_g, hs_u)
+
+    def _gather_parts(self, x_s: torch.Tensor):
+        """Sequence-parallel forward all-gather of the normed input, overlapped with its
+        consumers: the shards are broadcast from their owners on the side stream in the
+        PLORA_TP_CHUNKS launch groups; returns (x_full, [(sub_pack, event)]) so the
+        column-parallel kernels of a group start as soon as its rows arrived -- or
+        (x_full, None) after a plain all-gather when the tile lists cannot be cut at
+        the shard boundaries."""
+        if not self.sp:
+            return x_s, None
+        groups = self.meta.shard_launches_rows(self.shard.world, self.tp_chunks)
+        if groups is None or x_s.shape[1] % 8:
+            return self._gather(x_s), None
+        cur = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        side = self._side
+        x = torch.empty((self.T, x_s.shape[1]), dtype=x_s.dtype, device=self.device)
+        x[self.r0:self.r0 + self.Tl].copy_(x_s)
+        side.wait_stream(cur)
+        parts = []
+        with torch.cuda.stream(side):
+            for sub, shards in groups:
+                for owner, r0, r1 in shards:
+                    self.tp.broadcast_(x[r0:r1], owner)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                parts.append((sub, ev))
+        x.record_stream(side)
+        return x, parts
 
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
         """Backward of targets sharing the input x: per target K4 dH and K3 dB; ONE grouped
@@ -460,9 +521,9 @@ class PackedLoraTrainer:
             x1, rstd1 = ew.rmsnorm_fwd(h, lw["attn_norm"], cfg.norm_eps)
         else:
             h, x1, rstd1 = ew.add_rmsnorm_fwd(h_prev, delta, lw["attn_norm"], cfg.norm_eps)
-        x1 = self._gather(x1)     # sequence parallel: the rank's token shard -> all T rows
+        x1, parts = self._gather_parts(x1)   # sequence parallel: the token shards -> all T rows
         biases = [lw["q_bias"], lw["k_bias"], lw["v_bias"]] if cfg.qkv_bias else None   # added in the epilogue
-        (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1, biases)
+        (q, k, v), (hs_q, hs_k, hs_v) = self._group_fwd(layer, ("q", "k", "v"), x1, biases, parts)
         x1_keep = x1 if self.save_normed else None
         del x1
         ew.rope(q.view(B, s, H, hd), self.cos, self.sin, s, out=q)        # in place
@@ -476,17 +537,11 @@ class PackedLoraTrainer:
         o_out, hs_o = self._row_fwd(layer, "o", attn, lw["o"])   # TP: Y and Hs all-reduced (row-parallel)
         h_mid, x2, rstd2 = ew.add_rmsnorm_fwd(h, o_out, lw["mlp_norm"], cfg.norm_eps)
         del o_out
-        x2 = self._gather(x2)
+        x2, parts = self._gather_parts(x2)
         if self._fuse_swiglu:   # gate/up GEMM with the SwiGLU forward in its epilogue
-            bank, meta = self.bank, self.meta
-            hs_g = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
-            hs_u = torch.empty_like(hs_g)
-            ops.shrink_multi(meta, x2, [bank.shadow_of(layer, "gate", "A"), bank.shadow_of(layer, "up", "A")],
-                             [hs_g, hs_u])
-            g, u, act = ops.linear_gate_up_swiglu(meta, x2, lw["gate"], lw["up"], bank.shadow_of(layer, "gate", "B"),
-                                                  bank.shadow_of(layer, "up", "B"), hs_g, hs_u)
+            g, u, act, hs_g, hs_u = self._gate_up_swiglu(layer, x2, parts)
         else:
-            (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2)
+            (g, u), (hs_g, hs_u) = self._group_fwd(layer, ("gate", "up"), x2, parts=parts)
             act = ew.swiglu_fwd(g, u)
         x2_keep = x2 if self.save_normed else None
         del x2

@@ -199,12 +199,13 @@ def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
 
 
 def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmajor: bool = True,
-                        biases=None) -> list:
+                        biases=None, y_outs=None) -> list:
     """K1 + K2b for targets sharing x (q/k/v, gate/up) in ONE pair-GEMM launch:
     y_j = x op(W_j) + Hs_j,i B_j,i (+ bias_j, in the epilogue) (returns the new y_j [T][k_j])."""
     T, d = x.shape
     ks = [w.shape[0] if w_kmajor else w.shape[1] for w in ws]
-    ys = [torch.empty((T, k), dtype=torch.bfloat16, device=x.device) for k in ks]
+    ys = list(y_outs) if y_outs is not None else [torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
+                                                   for k in ks]
     karr = (ctypes.c_int64 * len(ks))(*ks)
     t = _TIMER.start() if _TIMER else None
     wp, _k1 = _ptr_array(ws, "w")
@@ -229,14 +230,18 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
 
 
 def linear_gate_up_swiglu(meta: PackMeta, x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor,
-                          bt_gate: torch.Tensor, bt_up: torch.Tensor, hs_gate: torch.Tensor, hs_up: torch.Tensor):
+                          bt_gate: torch.Tensor, bt_up: torch.Tensor, hs_gate: torch.Tensor, hs_up: torch.Tensor,
+                          outs=None):
     """gate/up K1+K2b in one launch with the SwiGLU forward in the epilogue: returns
     (g, u, act), act = silu(g) u bit-identical to elementwise.swiglu_fwd(g, u)."""
     T, d = x.shape
     ffn = w_gate.shape[0]
-    g = torch.empty((T, ffn), dtype=torch.bfloat16, device=x.device)
-    u = torch.empty_like(g)
-    act = torch.empty_like(g)
+    if outs is not None:
+        g, u, act = outs
+    else:
+        g = torch.empty((T, ffn), dtype=torch.bfloat16, device=x.device)
+        u = torch.empty_like(g)
+        act = torch.empty_like(g)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_linear_gate_up_swiglu(
         _stream(), ctypes.byref(meta.struct), _need(x, "x"), d, ffn, _need(w_gate, "w_gate"), _need(w_up, "w_up"),

@@ -84,7 +84,8 @@ class Comm:
       all_reduce_(t)           t = sum_r t_r (or max)
       all_gather_(out, inp)    out = concat_r inp_r (rank order, along dim 0)
       reduce_scatter_(out, inp) out = sum_r inp_r[rank block]
-      reduce_(t, root)         t on `root` = sum_r t_r (other ranks: unspecified)"""
+      reduce_(t, root)         t on `root` = sum_r t_r (other ranks: unspecified)
+      broadcast_(t, root)      t = t_root"""
     rank: int = 0
     world: int = 1
 
@@ -98,6 +99,9 @@ class Comm:
         raise NotImplementedError
 
     def reduce_(self, t: torch.Tensor, root: int) -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+    def broadcast_(self, t: torch.Tensor, root: int) -> torch.Tensor:  # pragma: no cover
         raise NotImplementedError
 
 
@@ -128,6 +132,11 @@ class DistComm(Comm):
     def reduce_(self, t, root):
         d = self._dist
         d.reduce(t, dst=d.get_global_rank(self.group, root) if self.group is not None else root, group=self.group)
+        return t
+
+    def broadcast_(self, t, root):
+        d = self._dist
+        d.broadcast(t, src=d.get_global_rank(self.group, root) if self.group is not None else root, group=self.group)
         return t
 
 
@@ -186,6 +195,13 @@ class AbiNcclComm(Comm):
         self._lib.check(self._lib.lib().plora_tp_reduce(
             torch.cuda.current_stream().cuda_stream, self._comm, t.data_ptr(), t.numel(), self._DT[t.dtype], root),
             "plora_tp_reduce")
+        return t
+
+    def broadcast_(self, t, root):
+        self._check(t)
+        self._lib.check(self._lib.lib().plora_tp_broadcast(
+            torch.cuda.current_stream().cuda_stream, self._comm, t.data_ptr(), t.numel(), self._DT[t.dtype], root),
+            "plora_tp_broadcast")
         return t
 
     def _check(self, *ts):
@@ -259,6 +275,10 @@ class ThreadComm(Comm):
 
     def reduce_(self, t, root):
         self._exchange(t, self._sum, lambda r: t.copy_(r) if self.rank == root else None)
+        return t
+
+    def broadcast_(self, t, root):
+        self._exchange(t, lambda sl: sl[root].clone(), t.copy_)
         return t
 
 

@@ -46,6 +46,9 @@ class NullComm(Comm):
     def reduce_(self, t, root):
         return t
 
+    def broadcast_(self, t, root):
+        return t
+
 
 def time_shard(cfg, specs, s, tp, steps, warmup):
     tr = PackedLoraTrainer(cfg, specs, s, device="cuda", tp=NullComm(0, tp))
