@@ -64,9 +64,11 @@ def _base(model_name: str, device: str):
 
 
 def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, steps_override: int | None = None,
-                     warmup: int = 1, tp=None) -> tuple:
+                     warmup: int = 1, tp=None, checkpoint_dir=None) -> tuple:
     """Run one packed job on ``device`` (its TP shard when ``tp`` is a communicator over
-    the job's ranks): returns (steps, seconds, mean iteration seconds, losses)."""
+    the job's ranks): returns (steps, seconds, mean iteration seconds, losses).  With
+    ``checkpoint_dir`` every configuration's adapter is written to the checkpoint pool
+    (checkpoint.py) when the job ends."""
     import torch
 
     from ..model import PRESETS, AdapterSpec, PackedLoraTrainer
@@ -88,6 +90,11 @@ def train_packed_job(job, configs_by_id: dict, model_name: str, device: str, ste
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     out = tuple(float(x) for x in losses.tolist())
+    if checkpoint_dir is not None:
+        from ..checkpoint import save_adapter
+
+        for i, c in enumerate(cfgs):
+            save_adapter(trainer, i, checkpoint_dir, config_id=c.id, extra={"job_id": job.id, "degree": job.degree})
     del trainer
     torch.cuda.empty_cache()
     return steps, dt, dt / steps, out
@@ -121,7 +128,7 @@ def tp_groups(queue: JobQueue, placement: Placement, world: int, gpu_count: int,
 def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, rank: int = 0, world: int = 1,
             model_name: str = "llama-3.1-8b", run_job: Callable | None = None,
             steps_override: int | None = None, all_gather: Callable | None = None,
-            new_group: Callable | None = None) -> dict:
+            new_group: Callable | None = None, checkpoint_dir=None) -> dict:
     """Execute this rank's share of the queue.  Returns a report with the per-job records
     (gathered from every rank when ``all_gather`` is given), profile records, the
     measured makespan (max over ranks of the per-device busy time) and the placement."""
@@ -138,7 +145,7 @@ def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, r
             extra = {"tp": comm} if comm is not None else {}
             if run_job is None:
                 steps, dt, it, losses = train_packed_job(job, by_id, model_name, f"cuda:{dev % max(1, _ndev())}",
-                                                         steps_override, **extra)
+                                                         steps_override, checkpoint_dir=checkpoint_dir, **extra)
             else:
                 steps, dt, it, losses = run_job(job, by_id, dev, **extra)
             records.append(JobRecord(job.id, dev, job.configs, steps, clock, dt, it, tuple(losses)))

@@ -32,3 +32,25 @@ def test_export_import_round_trip(tmp_path):
     l_packed = tr.forward_backward(tok)[2].item()
     l_solo = fresh.forward_backward(tok[r0:r1].contiguous())[0].item()
     assert abs(l_packed - l_solo) <= 1e-3 * abs(l_packed)
+
+
+def test_checkpoint_pool_files_round_trip(tmp_path):
+    """save_adapter writes PEFT files (safetensors + adapter_config.json with
+    lora_alpha = raw alpha * r); restore_adapter into a solo trainer reproduces the
+    adapter's packed loss."""
+    from paper_2508_02932_b200.checkpoint import load_adapter, restore_adapter, save_adapter
+    specs, s = bench_adapters("tiny")
+    tr = PackedLoraTrainer(PRESETS["tiny"], specs, s, device="cuda")
+    tok = tr.synthetic_tokens().cuda()
+    for _ in range(2):
+        tr.step(tok)
+    out = save_adapter(tr, 1, tmp_path, config_id="cfg-1")
+    state, cfg = load_adapter(out)
+    assert cfg["r"] == specs[1].rank and cfg["lora_alpha"] == specs[1].alpha * specs[1].rank
+    assert cfg["optimizer_steps"] == 2 and len(cfg["target_modules"]) == 7
+    solo = PackedLoraTrainer(PRESETS["tiny"], [specs[1]], s, device="cuda", base=tr.base)
+    restore_adapter(solo, 0, state)
+    r0, r1 = tr.meta.row_offsets[1], tr.meta.row_offsets[2]
+    l_packed = tr.forward_backward(tok)[1].item()
+    l_solo = solo.forward_backward(tok[r0:r1].contiguous())[0].item()
+    assert abs(l_packed - l_solo) <= 1e-3 * abs(l_packed)

@@ -142,3 +142,21 @@ def test_abi_nccl_comm_single_rank():
             assert torch.equal(x, y) and torch.equal(x, g) and torch.equal(x, r)
     finally:
         comm.close()
+
+
+def test_tp_checkpoint_gathers_full_adapters():
+    """checkpoint.adapter_state on a TP group (collective all-gather of the sharded
+    factors) == the unsharded trainer's adapter, exactly."""
+    from paper_2508_02932_b200.checkpoint import adapter_state
+    ref = _make("tiny-qwen")
+    want = [adapter_state(ref, i) for i in range(ref.meta.n_adapters)]
+
+    def rank_fn(comm):
+        tr = _make("tiny-qwen", tp=comm)
+        return [adapter_state(tr, i) for i in range(tr.meta.n_adapters)]
+
+    for states in run_threaded(2, rank_fn):
+        for got, exp in zip(states, want):
+            assert got.keys() == exp.keys()
+            for k in exp:
+                assert torch.equal(got[k], exp[k]), k
