@@ -211,7 +211,7 @@ class PackedLoraTrainer:
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
-                 save_normed: bool | None = None, sequence_parallel: bool = True):
+                 save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool | None = None):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
@@ -261,6 +261,11 @@ class PackedLoraTrainer:
         self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
         self.tp_chunks = int(os.environ.get("PLORA_TP_CHUNKS", "4"))   # TP all-reduce / GEMM overlap depth
         self._side = None
+        # fused GEMM + reduce onto owners through peer memory (opt-in, see _fused_reduce)
+        if tp_fused is None:
+            tp_fused = os.environ.get("PLORA_TP_FUSED", "0") == "1"
+        self.tp_fused = bool(tp_fused and self.sp and getattr(self.tp, "supports_peer_memory", False))
+        self._peer = {}
         # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
         self._fuse_swiglu = self.targets[4].h_out >= 256 and os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
@@ -301,7 +306,9 @@ class PackedLoraTrainer:
         ops.shrink(meta, x, bank.shadow_of(layer, tname, "A"), hs)
         y_part = torch.empty((self.T, w.shape[0]), dtype=bf16, device=self.device)
         bt = bank.shadow_of(layer, tname, "B")
-        y = self._overlapped(lambda m: ops.linear_expand(m, x, w, True, bt, hs, y_out=y_part), y_part, extra=(hs,))
+        y = self._overlapped(lambda m, out=y_part: ops.linear_expand(m, x, w, True, bt, hs, y_out=out,
+                                                                     residual=None if out is y_part else out),
+                             y_part, extra=(hs,))
         return y, hs
 
     def _overlapped(self, launch, y: torch.Tensor, extra=()):
@@ -319,6 +326,8 @@ class PackedLoraTrainer:
         side = self._side
         wide = y.shape[1] >= 256   # pair-GEMM path (sub-packs only restrict pair tiles)
         out = y
+        if self.tp_fused and wide and self.meta.shard_tile_chunks(self.shard.world) is not None:
+            return self._fused_reduce(launch, y, extra)
         if self.sp:
             chunks = self.meta.shard_launches(self.shard.world, self.tp_chunks) if wide else None
             if chunks is None:
@@ -378,6 +387,34 @@ class PackedLoraTrainer:
             return pre[1]
         torch.cuda.current_stream().wait_event(pre[2])
         return pre[1]
+
+    def _fused_reduce(self, launch, y: torch.Tensor, extra=()):
+        """Row-parallel GEMM fused with the reduce onto the owning rank, over peer memory:
+        every rank runs the GEMM tiles of owner c's token shard with its epilogue in
+        reduce-add mode aimed at owner c's buffer (a TMA reduce-add of each finished
+        bf16 tile into the peer's memory over NVLink), so the transfer rides the GEMM tile
+        by tile and no separate collective touches the data.  Owners zero their rows, a
+        barrier, the GEMMs (owners visited in rank-rotated order to spread the links),
+        a barrier; the owner's rows are its shard of the sum.  Two buffers per width
+        alternate (the consumer of one output runs before the buffer is reused)."""
+        d = y.shape[1]
+        slot = self._peer.setdefault(("next", d), 0)
+        self._peer[("next", d)] = slot ^ 1
+        if (d, slot) not in self._peer:
+            self._peer[(d, slot)] = self.tp.peer_buffers((self.T, d), y.dtype)
+        buf, peers = self._peer[(d, slot)]
+        chunks = self.meta.shard_tile_chunks(self.shard.world)
+        own = buf[self.r0:self.r0 + self.Tl]
+        own.zero_()
+        self.tp.barrier_()
+        g, r = self.shard.world, self.shard.rank
+        for j in range(g):
+            c = (r + j) % g
+            launch(chunks[c][0], peers[c])      # epilogue: reduce-add into rank c's rows
+        self.tp.barrier_()
+        for t in extra:
+            self.tp.all_reduce_(t)
+        return own
 
     def _gather(self, x_s: torch.Tensor) -> torch.Tensor:
         """Sequence parallelism: every rank's [T/tp][d] token shard -> the full [T][d]."""
@@ -484,7 +521,8 @@ class PackedLoraTrainer:
         if need_dx and self.tp is not None:   # partial dX_s: chunked all-reduce overlapping the GEMM
             dx_part = torch.empty((self.T, x.shape[1]), dtype=bf16, device=self.device)
             dx = self._overlapped(
-                lambda m: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=dx_part),
+                lambda m, out=dx_part: ops.linear_dx_group(m, list(dys), ws, ashs, dhs, x.shape[1], dx_out=out,
+                                                           dx_residual=None if out is dx_part else out),
                 dx_part, extra=dhs)
         else:
             if need_dx:   # K6 (Case 4) for every target in one accumulator

@@ -104,6 +104,19 @@ class Comm:
     def broadcast_(self, t: torch.Tensor, root: int) -> torch.Tensor:  # pragma: no cover
         raise NotImplementedError
 
+    # Peer memory for the fused GEMM + reduce (model.PackedLoraTrainer tp_fused): every
+    # rank allocates a buffer of the same shape and gets device views of all ranks' copies.
+    supports_peer_memory = False
+
+    def peer_buffers(self, shape, dtype):  # pragma: no cover
+        """(this rank's buffer, [view of rank r's buffer for r in group])."""
+        raise NotImplementedError
+
+    def barrier_(self) -> None:  # pragma: no cover
+        """Stream-ordered barrier over the group (all ranks' prior work on their current
+        streams is complete -- and visible -- before any rank's later work starts)."""
+        raise NotImplementedError
+
 
 class DistComm(Comm):
     """torch.distributed process group (backend nccl on GPU, gloo on CPU)."""
@@ -138,6 +151,20 @@ class DistComm(Comm):
         d = self._dist
         d.broadcast(t, src=d.get_global_rank(self.group, root) if self.group is not None else root, group=self.group)
         return t
+
+    supports_peer_memory = True
+
+    def peer_buffers(self, shape, dtype):
+        """torch symmetric memory (CUDA IPC over NVLink): each rank maps every peer's copy."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        buf = symm_mem.empty(tuple(shape), dtype=dtype, device=torch.cuda.current_device())
+        group = self.group if self.group is not None else self._dist.group.WORLD
+        self._symm = symm_mem.rendezvous(buf, group)
+        return buf, [self._symm.get_buffer(r, tuple(shape), dtype) for r in range(self.world)]
+
+    def barrier_(self):
+        self._symm.barrier(channel=0)
 
 
 class AbiNcclComm(Comm):
@@ -280,6 +307,22 @@ class ThreadComm(Comm):
     def broadcast_(self, t, root):
         self._exchange(t, lambda sl: sl[root].clone(), t.copy_)
         return t
+
+    supports_peer_memory = True
+
+    def peer_buffers(self, shape, dtype):
+        """Threads share one device: the 'peers' are the other ranks' buffers on it."""
+        g = self.g
+        buf = torch.empty(tuple(shape), dtype=dtype, device=torch.cuda.current_device())
+        g.slots[self.rank] = buf
+        g.barrier.wait()
+        peers = list(g.slots)
+        g.barrier.wait()
+        return buf, peers
+
+    def barrier_(self):
+        torch.cuda.current_stream().synchronize()
+        self.g.barrier.wait()
 
 
 def run_threaded(world: int, fn: Callable[[Comm], object]) -> list:

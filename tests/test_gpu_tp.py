@@ -19,11 +19,11 @@ from paper_2508_02932_b200.tp import TPShard, run_threaded
 pytestmark = pytest.mark.gpu
 
 
-def _make(preset, tp=None, sp=True, save_normed=None):
+def _make(preset, tp=None, sp=True, save_normed=None, fused=False):
     cfg = PRESETS[preset]
     specs, s = bench_adapters(preset)
     return PackedLoraTrainer(cfg, specs, s, device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in specs],
-                             tp=tp, sequence_parallel=sp, save_normed=save_normed)
+                             tp=tp, sequence_parallel=sp, save_normed=save_normed, tp_fused=fused)
 
 
 def _grads(tr):
@@ -45,22 +45,25 @@ def _masters(tr):
             for i in range(tr.meta.n_adapters)}
 
 
-@pytest.mark.parametrize("preset,g,sp,keep", [("tiny-qwen", 2, True, True), ("tiny", 4, True, True),
-                                              ("tiny-qwen", 2, True, False), ("tiny-qwen", 2, False, True),
-                                              ("tiny", 4, False, True)])
-def test_tp_matches_unsharded(preset, g, sp, keep):
+@pytest.mark.parametrize("preset,g,sp,keep,fused", [("tiny-qwen", 2, True, True, False), ("tiny", 4, True, True, False),
+                                                    ("tiny-qwen", 2, True, False, False),
+                                                    ("tiny-qwen", 2, False, True, False),
+                                                    ("tiny", 4, False, True, False), ("tiny-qwen", 2, True, True, True)])
+def test_tp_matches_unsharded(preset, g, sp, keep, fused):
     """sp: Megatron sequence parallelism (token-sharded residual stream; g = 2 cuts the
     pair-tile list exactly at the shard boundaries -> per-shard reduces overlapping the
     GEMM; g = 4 does not -> one reduce-scatter); sp = False: all-reduce chunks.
-    keep = False: the normed inputs are re-gathered in the backward on the side stream."""
+    keep = False: the normed inputs are re-gathered in the backward on the side stream.
+    fused: the row-parallel GEMMs reduce their tiles straight into the owning rank's
+    buffer (TMA reduce-add into peer memory -- here the other threads' buffers)."""
     ref = _make(preset)
     tokens = ref.synthetic_tokens().cuda()
     ref_losses = ref.forward_backward(tokens).double().cpu()
     ref_grads = _grads(ref)
 
     def rank_fn(comm):
-        tr = _make(preset, tp=comm, sp=sp, save_normed=keep)
-        assert tr.sp == sp
+        tr = _make(preset, tp=comm, sp=sp, save_normed=keep, fused=fused)
+        assert tr.sp == sp and tr.tp_fused == fused
         losses = tr.forward_backward(tokens).double().cpu()
         grads = _grads(tr)
         tr.bank.adamw_step()
@@ -92,7 +95,7 @@ def test_tp_matches_unsharded(preset, g, sp, keep):
         num += e * e
         den += rn * rn
         worst = max(worst, e / max(rn, 1e-30))
-    print(f"tp={g} sp={sp} {preset}: worst per-block grad rel-Frob {worst:.3e}, pooled {(num / den) ** 0.5:.3e}")
+    print(f"tp={g} sp={sp} fused={fused} {preset}: worst per-block grad rel-Frob {worst:.3e}, pooled {(num / den) ** 0.5:.3e}")
     assert worst <= 3e-2
     assert (num / den) ** 0.5 <= 2e-2
 
