@@ -26,11 +26,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _make(tp=None, save_normed=None):
+def _make(tp=None, save_normed=None, fused=False):
     cfg = PRESETS["tiny-qwen"]
     specs, s = bench_adapters("tiny-qwen")
     return PackedLoraTrainer(cfg, specs, s, device="cuda", a_scale=0.05, b_std=[0.2 / x.alpha for x in specs],
-                             tp=tp, save_normed=save_normed)
+                             tp=tp, save_normed=save_normed, tp_fused=fused)
 
 
 def _grads(tr):
@@ -40,12 +40,12 @@ def _grads(tr):
             for i in range(tr.meta.n_adapters)}
 
 
-def _worker(rank, world, port, keep, out):
+def _worker(rank, world, port, keep, fused, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    tr = _make(DistComm(), save_normed=keep)
-    assert tr.sp
+    tr = _make(DistComm(), save_normed=keep, fused=fused)
+    assert tr.sp and tr.tp_fused == fused
     tokens = tr.synthetic_tokens().cuda()
     losses = tr.forward_backward(tokens).double().cpu()
     grads = _grads(tr)
@@ -56,8 +56,11 @@ def _worker(rank, world, port, keep, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("keep", [True, False])
-def test_tp2_two_processes_gloo(keep):
+@pytest.mark.parametrize("keep,fused", [(True, False), (False, False)])
+def test_tp2_two_processes_gloo(keep, fused):
+    """(The fused peer-memory path is not covered here: torch symmetric memory refuses two
+    ranks on one device -- "allocations from overlapping devices"; test_gpu_tp.py covers
+    it with thread-emulated ranks.)"""
     ref = _make()
     tokens = ref.synthetic_tokens().cuda()
     ref_losses = ref.forward_backward(tokens).double().cpu()
@@ -66,7 +69,7 @@ def test_tp2_two_processes_gloo(keep):
     torch.cuda.empty_cache()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), keep, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), keep, fused, out), nprocs=2, join=True)
     (l0, g0, m0), (l1, g1, m1) = out[0], out[1]
     assert torch.equal(l0, l1)
     assert ((l0 - ref_losses).abs() / ref_losses.abs()).max().item() <= 1e-2
