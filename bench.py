@@ -142,6 +142,45 @@ def cpu_reference(cfg_name: str, frac: float | None = None) -> dict:
             "host_cpus": os.cpu_count()}
 
 
+def dropin_api_sample(cfg_name: str) -> dict:
+    """The reference-facing operator API itself (paper_2508_02932_b200.lorapack:
+    pack_adapters -> packed_forward -> packed_backward, float64 numpy in and out, the
+    device path in between) on the SAME sample as cpu_baseline (7 LoRA linears of one
+    layer at 1/16 of the step's tokens), scaled by 1/L the same way -- an API-for-API
+    comparison with the reference arm.  The drop-in is stateless (base weight and
+    adapters cross PCIe on every call, as numpy arrays in the reference signature), so
+    it is transfer-bound; the training path keeps everything resident."""
+    import numpy as np
+
+    from paper_2508_02932_b200 import lorapack as L
+    from paper_2508_02932_b200.model import PRESETS, bench_adapters
+
+    cfg = PRESETS[cfg_name]
+    specs, s = bench_adapters(cfg_name)
+    frac = {"tiny": 1.0, "qwen2.5-3b": 1 / 8, "llama-3.1-8b": 1 / 16, "qwen2.5-32b": 1 / 32}[cfg_name]
+    rng = np.random.default_rng(0)
+    toks = [max(1, int(sp.batch * s * frac)) for sp in specs]
+    T = sum(toks)
+    work = []
+    for t in cfg.targets():
+        ads = [L.AdapterWeights(rng.uniform(-1, 1, (t.h_in, sp.rank)) / np.sqrt(t.h_in),
+                                rng.standard_normal((sp.rank, t.h_out)) * 0.02, sp.alpha) for sp in specs]
+        xs = [rng.standard_normal((n, t.h_in)) for n in toks]
+        dys = [rng.standard_normal((n, t.h_out)) for n in toks]
+        work.append((ads, xs, rng.standard_normal((t.h_in, t.h_out)) * 0.02, dys))
+    ads, xs, w, dys = work[0]
+    L.packed_backward(L.pack_adapters(ads, xs), w, dys)   # warm-up (library load, first launches)
+    t0 = time.perf_counter()
+    for ads, xs, w, dys in work:
+        packed = L.pack_adapters(ads, xs)
+        L.packed_forward(packed, w)
+        L.packed_backward(packed, w, dys)
+    dt = time.perf_counter() - t0
+    return {"value": T / (dt * cfg.n_layers), "unit": "tokens/s",
+            "sample": f"lorapack drop-in (numpy fp64 in/out), same 7-linear {T}-token sample as cpu_baseline, "
+                      f"{dt:.2f} s, scaled by 1/L"}
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -340,6 +379,7 @@ def main() -> None:
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(args.config)
+        line["dropin_api"] = dropin_api_sample(args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
