@@ -19,7 +19,7 @@ __all__ = [
     "WorkloadSyntaxError", "WorkloadValidationError", "TargetModule", "ModelSpec", "GpuPool",
     "ShardingSpec", "LoraConfig", "ProfileRecord", "WorkloadSpec", "config_id", "enumerate_grid",
     "validate_config", "validate_model", "validate_pool", "validate_sharding", "parse_workload",
-    "serialize_workload", "workload_digest", "model_spec_from_config",
+    "serialize_workload", "workload_digest", "model_spec_from_config", "STATE_BYTES_PLORA",
 ]
 
 MAX_TARGETS = 7
@@ -53,6 +53,11 @@ class ModelSpec:
     embed_act_coeff: float = 0.0
     attn_act_coeff: float = 0.0
     mlp_act_coeff: float = 0.0
+    # B200 extension (default: the reference's c_prec for
+    # everything): bytes per adapter parameter of (params, grads, one optimizer moment).
+    # The packed trainer keeps fp32 masters + a bf16 shadow, fp32 grads and fp32 AdamW
+    # moments: (6, 4, 4) -- see STATE_BYTES_PLORA.
+    state_bytes: tuple | None = None
 
     @property
     def act_coeff_sum(self) -> float:
@@ -175,6 +180,8 @@ def validate_model(model: ModelSpec) -> list:
         errs.append("base_param_count must be >= 0")
     if model.c_prec < 1:
         errs.append(f"c_prec must be a positive byte count (got {model.c_prec})")
+    if model.state_bytes is not None and (len(model.state_bytes) != 3 or min(model.state_bytes) < 1):
+        errs.append(f"state_bytes must be three positive byte counts (got {model.state_bytes})")
     for attr in ("embed_act_coeff", "attn_act_coeff", "mlp_act_coeff"):
         if getattr(model, attr) < 0:
             errs.append(f"{attr} must be >= 0")
@@ -204,13 +211,17 @@ def validate_sharding(shard: ShardingSpec) -> list:
     return errs
 
 
-def model_spec_from_config(cfg, c_prec: int = 2, act_coeffs=(0.0, 0.0, 0.0)) -> ModelSpec:
-    """ModelSpec of a ``model.ModelConfig`` preset (all 7 LoRA targets)."""
+STATE_BYTES_PLORA = (6, 4, 4)   # fp32 master + bf16 shadow, fp32 grad, fp32 m / v (adapters.py)
+
+
+def model_spec_from_config(cfg, c_prec: int = 2, act_coeffs=(0.0, 0.0, 0.0), state_bytes=None) -> ModelSpec:
+    """ModelSpec of a ``model.ModelConfig`` preset (all 7 LoRA targets); pass
+    ``state_bytes=STATE_BYTES_PLORA`` to cost adapter state as the packed trainer stores it."""
     targets = tuple(TargetModule(t.name, t.h_in, t.h_out) for t in cfg.targets())
     base = cfg.n_layers * sum(t.h_in * t.h_out for t in cfg.targets()) + cfg.vocab * cfg.d * (1 if cfg.tied else 2)
     return ModelSpec(name=cfg.name, n_layers=cfg.n_layers, target_modules=targets, base_param_count=base,
                      c_prec=c_prec, embed_act_coeff=act_coeffs[0], attn_act_coeff=act_coeffs[1],
-                     mlp_act_coeff=act_coeffs[2])
+                     mlp_act_coeff=act_coeffs[2], state_bytes=tuple(state_bytes) if state_bytes else None)
 
 
 # ------------------------------------------------------------------ document I/O
@@ -236,6 +247,16 @@ def _field(obj: Mapping, key: str, kind, where: str, default=...):
     return v
 
 
+def _state_bytes(m: Mapping):
+    """Optional model.state_bytes (B200 extension): [param, grad, optimizer-moment] bytes."""
+    if "state_bytes" not in m:
+        return None
+    v = m["state_bytes"]
+    if not (isinstance(v, list) and len(v) == 3 and all(isinstance(x, int) and not isinstance(x, bool) for x in v)):
+        raise WorkloadValidationError("model: state_bytes must be a list of three integers")
+    return tuple(v)
+
+
 def parse_workload(text: str) -> WorkloadSpec:
     """Parse a workload JSON document (reference workload.py:415-450)."""
     try:
@@ -254,7 +275,8 @@ def parse_workload(text: str) -> WorkloadSpec:
     co = _field(m, "activation_coeffs", dict, "model", {})
     model = ModelSpec(_field(m, "name", str, "model"), _field(m, "n_layers", int, "model"), tuple(targets),
                       _field(m, "base_param_count", int, "model"), _field(m, "c_prec", int, "model"),
-                      *(_field(co, k, float, "model.activation_coeffs", 0.0) for k in ("embed", "attn", "mlp")))
+                      *(_field(co, k, float, "model.activation_coeffs", 0.0) for k in ("embed", "attn", "mlp")),
+                      state_bytes=_state_bytes(m))
     if validate_model(model):
         raise WorkloadValidationError("model: " + "; ".join(validate_model(model)))
     p = _field(doc, "pool", dict, "workload")
@@ -319,7 +341,8 @@ def _as_doc(spec: WorkloadSpec) -> dict:
                   "target_modules": [{"name": t.name, "h_in": t.h_in, "h_out": t.h_out} for t in m.target_modules],
                   "base_param_count": m.base_param_count, "c_prec": m.c_prec,
                   "activation_coeffs": {"embed": m.embed_act_coeff, "attn": m.attn_act_coeff,
-                                        "mlp": m.mlp_act_coeff}},
+                                        "mlp": m.mlp_act_coeff},
+                  **({"state_bytes": list(m.state_bytes)} if m.state_bytes else {})},
         "pool": {"gpu_count": spec.pool.gpu_count, "mem_per_gpu": spec.pool.mem_per_gpu,
                  "load_factor": spec.pool.load_factor},
         "configs": [{"id": c.id, "rank": c.rank, "alpha": c.alpha, "batch_size": c.batch_size,

@@ -150,3 +150,33 @@ def test_balance_extension_beats_reference_dtm_on_token_linear_cost():
     t_bal = S.place(bal_q, 8).makespan
     assert t_bal <= S.place(ref_q, 8).makespan + 1e-9
     assert t_bal <= S.place(S.min_gpu_queue(configs, 8, tm, mem), 8).makespan + 1e-9
+
+
+def test_state_bytes_extension_costs_adapter_state_at_trainer_precision():
+    """B200 extension: ModelSpec.state_bytes = (6, 4, 4) costs an
+    adapter parameter at 6 + 4 + 2*4 = 18 B (the packed trainer's fp32 master + bf16
+    shadow, fp32 grad, fp32 moments) instead of 4 * c_prec; activations keep c_prec;
+    unset, the reference numbers are unchanged; the workload document round-trips."""
+    from paper_2508_02932_b200 import sweep as S
+    from paper_2508_02932_b200.model import PRESETS
+    cfg = PRESETS["llama-3.1-8b"]
+    ref = S.model_spec_from_config(cfg, c_prec=2)
+    ext = S.model_spec_from_config(cfg, c_prec=2, state_bytes=S.STATE_BYTES_PLORA)
+    lc = S.LoraConfig("c", 16, 32.0, 2, 1e-4, 1024, 50)
+    shard = S.ShardingSpec.tensor_parallel(1)
+    n = cfg.n_layers * 16 * sum(t.h_in + t.h_out for t in cfg.targets())
+    a = S.lora_state_memory(lc, ref, shard)
+    b = S.lora_state_memory(lc, ext, shard)
+    assert (a.param_bytes, a.grad_bytes, a.opt_bytes) == (2 * n, 2 * n, 4 * n)
+    assert (b.param_bytes, b.grad_bytes, b.opt_bytes) == (6 * n, 4 * n, 8 * n)
+    assert a.act_bytes == b.act_bytes
+    # TP degree 8 divides every component
+    b8 = S.lora_state_memory(lc, ext, S.ShardingSpec.tensor_parallel(8))
+    assert b8.param_bytes == -(-6 * n // 8)
+    # workload documents: absent key -> reference layout, present -> round trip
+    pool = S.GpuPool(8, int(178e9))
+    for m in (ref, ext):
+        doc = S.serialize_workload(S.WorkloadSpec(m, pool, (lc,), ()))
+        assert ("state_bytes" in doc) == (m.state_bytes is not None)
+        assert S.parse_workload(doc).model == m
+    assert S.validate_model(S.ModelSpec("m", 1, ref.target_modules, 1, 2, state_bytes=(6, 0, 4)))

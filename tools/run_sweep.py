@@ -46,7 +46,10 @@ def main():
     configs = grid()
     by_id = {c.id: c for c in configs}
     # memory model: bf16 base; activations ~2.95 MB/token saved by the trainer (measured peak at T=32768)
-    model = S.model_spec_from_config(cfg, c_prec=2, act_coeffs=(0.0, 2.95e6 / 2 / 2, 2.95e6 / 2 / 2))
+    # adapter state at the trainer's storage precision (fp32 master + bf16 shadow, fp32 grad / moments);
+    # on this grid the plans are identical to the reference's c_prec costing (activations dominate)
+    model = S.model_spec_from_config(cfg, c_prec=2, act_coeffs=(0.0, 2.95e6 / 2 / 2, 2.95e6 / 2 / 2),
+                                     state_bytes=S.STATE_BYTES_PLORA)
     pool = S.GpuPool(args.gpus, int(args.mem_gb * 1e9), load_factor=0.9)
 
     # 1. profile packs of 1 .. 16 configs at degree 1
