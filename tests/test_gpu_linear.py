@@ -281,3 +281,36 @@ def test_grouped_expand_bias_epilogue(widths):
     refs = ops.linear_expand_group(meta, x, ws, bts, hss)
     for y, r, b in zip(ys, refs, bs):
         assert torch.equal(y, r + b)
+
+
+@pytest.mark.parametrize("d,k", [(4096, 14336), (14336, 4096)])
+def test_full_c3_size_packed_linear(d, k):
+    """BASELINE C3 at full size: the 16 bench adapters (ranks [8,16,32,64] x 4, batches
+    1..4 x 1024 tokens, T = 32,768) through the gate/up (d=4096 -> k=14336) and down
+    (14336 -> 4096) shapes, forward + backward, against the fp32 torch reference of the
+    same bf16 operands (the bf16 tier: rel-Frobenius <= 1e-2 for Y / dX, 5e-3 for dA / dB)."""
+    from paper_2508_02932_b200.model import bench_adapters
+    specs, s = bench_adapters("llama-3.1-8b")
+    ranks = [sp.rank for sp in specs]
+    tokens = [sp.batch * s for sp in specs]
+    meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, k, seed=d ^ k, kmajor=True)
+    assert meta.total_tokens == 32768
+    y, hs = ops.linear_fwd(meta, x, w, True, a_sh, bt_sh)
+    ga = torch.empty(d * meta.rpad16_total, device="cuda")
+    gb = torch.empty(k * meta.rpad16_total, device="cuda")
+    dx = ops.linear_bwd(meta, x, w, True, a_sh, bt_sh, hs, dy, ga, gb)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    ry, rdx, rdA, rdB = reference(meta, x, w, True, a_sh, bt_sh, dy)
+    assert rel(y, ry) < 1e-2 and rel(dx, rdx) < 1e-2
+    for i, r in enumerate(ranks):
+        rp = int(meta.rpad_off[i + 1] - meta.rpad_off[i])
+        blk_a = ga[d * int(meta.rpad_off[i]): d * int(meta.rpad_off[i + 1])].view(d, rp)
+        blk_b = gb[k * int(meta.rpad_off[i]): k * int(meta.rpad_off[i + 1])].view(k, rp)
+        assert rel(blk_a[:, :r], rdA[i]) < 5e-3, ("dA", i)
+        assert rel(blk_b[:, :r], rdB[i]) < 5e-3, ("dB", i)
+    # size-independent property: the LoRA part is linear in alpha -- doubling every alpha
+    # doubles Y - X W exactly up to the bf16 rounding of Hs (checked at the same tolerance)
+    meta2 = build_meta(ranks, tokens, [2 * a for a in meta.alphas]).to("cuda")
+    y2, _ = ops.linear_fwd(meta2, x, w, True, a_sh, bt_sh)
+    base = (x.float() @ w.float().t())
+    assert rel(y2.float() - base, 2 * (ry - base)) < 2e-2
