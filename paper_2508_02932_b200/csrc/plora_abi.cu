@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <queue>
+#include <atomic>
 #include <unordered_map>
 #include <vector>
 #include <string>
@@ -122,6 +123,20 @@ static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   return 0;
 }
 
+// Opt a kernel into its dynamic shared memory size on the current device (the attribute
+// is per device; the per-instantiation bit mask makes it once per device and thread-safe).
+template <typename K>
+static int ensure_smem(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  PLORA_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.fetch_or(bit, std::memory_order_release);
+  }
+  return 0;
+}
+
 static int num_sms() {
   static int cached[64] = {0};
   int dev = 0;
@@ -139,11 +154,8 @@ template <int BN, int MODE, bool B_MN>
 static int launch(const GemmArgs& args, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = plora_gemm_kernel<BN, MODE, B_MN>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
+  if (ensure_smem(kern, Cfg::kSmemBytes, configured)) return 1;
   const int total = args.n_groups * args.n_ntiles;
   if (total <= 0) return 0;
   const int grid = total < num_sms() ? total : num_sms();
@@ -167,11 +179,8 @@ static bool g_pair_enabled = [] {
 template <bool B_MN, int NB, int EPI = EPI_STORE>
 static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   auto kern = plora_gemm_pair_kernel<B_MN, NB, EPI>;
-  static bool configured = false;
-  if (!configured) {
-    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<NB>::kSmemBytes));
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
+  if (ensure_smem(kern, PairCfg<NB>::kSmemBytes, configured)) return 1;
   const int total = args.g.n_groups * args.g.n_ntiles;
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
@@ -452,11 +461,8 @@ template <int BN>
 static int launch_segred_lpt(const GemmArgs& args, const SegSched& sched, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = plora_segred_lpt_kernel<BN>;
-  static bool configured = false;
-  if (!configured) {
-    PLORA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
+  if (ensure_smem(kern, Cfg::kSmemBytes, configured)) return 1;
   kern<<<sched.n_ctas, kThreads, Cfg::kSmemBytes, stream>>>(args, sched);
   PLORA_CUDA(cudaGetLastError());
   return 0;
