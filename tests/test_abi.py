@@ -32,3 +32,18 @@ def test_device_check_fails_loudly_without_gpu():
         return
     assert _lib.lib().plora_device_check() != 0
     assert _lib.lib().plora_last_error()
+
+
+def test_invalid_arguments_return_status_and_message():
+    """Nothing throws across the ABI: a NULL or empty pack is
+    rejected with a nonzero status and a plora_last_error() message, before any CUDA call."""
+    import ctypes
+    lib = _lib.lib()
+    rc = lib.plora_linear_fwd(None, None, None, 64, 64, None, 1, None, None, None, None, 64, None)
+    assert rc != 0 and b"pack is NULL" in lib.plora_last_error()
+    empty = _lib.PackStruct()
+    rc = lib.plora_lora_segred(None, ctypes.byref(empty), 64, None, None, None)
+    assert rc != 0 and b"no adapters" in lib.plora_last_error()
+    rc = lib.plora_linear_bwd(None, None, None, 64, 64, None, 1, None, None, None, None, None, None, 64, None,
+                              None, None)
+    assert rc != 0 and b"pack is NULL" in lib.plora_last_error()
