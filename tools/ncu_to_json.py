@@ -24,8 +24,8 @@ KEYS = {
     "registers_per_thread": "launch__registers_per_thread",
     "grid": "launch__grid_size",
 }
-SCALE = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
-         "nsecond": 1e-3}
+SCALE = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+         "nsecond": 1e-3, "ns": 1e-3, "Tbyte": 1e12}
 
 raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
