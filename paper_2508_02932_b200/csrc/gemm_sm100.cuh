@@ -463,18 +463,21 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 // CTAs' empty / tmem_full barriers; both CTAs' epilogues drain their own 128 TMEM
 // lanes and arrive on the leader's tmem_empty barrier.  Pair tiles never straddle
 // adapters (meta builder), so the fused LoRA K-steps use one adapter's B_i.
-template <int NB>
+template <int NB, int EPI_ = 0>
 struct PairCfg {
   static constexpr int kBN = 256 * NB;                      // output columns per pair tile
   static constexpr int kABytes = kBM * kBK * 2;             // 16 KB (own 128 rows)
   static constexpr int kBBytes = NB * 128 * kBK * 2;        // own half of each 256-col chunk
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = NB == 1 ? 6 : 4;
+  // EPI_SWIGLU (= 2) stores three chunks per accumulator chunk pair: 3 stages, 4 staging
+  // buffers per epilogue warp instead of 4 stages / 2 buffers
+  static constexpr int kStages = NB == 1 ? 6 : (EPI_ == 2 ? 3 : 4);
+  static constexpr int kStgBufs = EPI_ == 2 ? 4 : 2;
   static constexpr int kAccStages = NB == 1 ? 2 : 1;
   static constexpr int kTmemCols = 512;
   static constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;      // producer + MMA + epilogue
-  static constexpr int kStgBytes = kEpiWarps * 2 * 2048;   // per warp: 2 x [32 rows x 32 bf16], SW64
+  static constexpr int kStgBytes = kEpiWarps * kStgBufs * 2048;   // per warp: kStgBufs x [32 rows x 32 bf16], SW64
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*barriers*/ + kStgBytes + 1024 /*align*/;
   static constexpr int kBand = 8;                           // pair tiles per raster band
 };
@@ -603,13 +606,14 @@ __device__ __forceinline__ uint32_t chunk_word(const PairOut& po, int col0, cons
   return pack_bf16x2(y.x + b0, y.y + b1);
 }
 
+template <int NBUF = 2>
 __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg, int& issued, int lane, int col0,
                                                 int m0, int m_len, const uint32_t (&v)[16]) {
   if (col0 >= po.N) return;
   if (m_len == 32) {
-    uint8_t* buf = stg + (issued & 1) * 2048;
-    if (issued >= 2) {
-      if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has read it
+    uint8_t* buf = stg + (issued % NBUF) * 2048;
+    if (issued >= NBUF) {
+      if (lane == 0) bulk_wait_read<NBUF - 1>();   // the store that last used this buffer has read it
       __syncwarp();
     }
 #pragma unroll
@@ -646,6 +650,7 @@ __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg,
 
 // EPI_SWIGLU: one gate chunk and the matching up chunk (bf16-packed) -> stores g, u and
 // act = silu(g) u from the bf16-rounded values (the arithmetic of swiglu_fwd_kernel).
+template <int NBUF>
 __device__ __forceinline__ void pair_emit_swiglu(const PairOut& pg, const PairOut& pu, const PairOut& pa, uint8_t* stg,
                                                  int& issued, int lane, int col0, int m0, int m_len,
                                                  const uint32_t (&vg)[16], const uint32_t (&vu)[16]) {
@@ -656,15 +661,15 @@ __device__ __forceinline__ void pair_emit_swiglu(const PairOut& pg, const PairOu
     const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vu[q]));
     va[q] = pack_bf16x2(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
   }
-  pair_emit_chunk(pg, stg, issued, lane, col0, m0, m_len, vg);
-  pair_emit_chunk(pu, stg, issued, lane, col0, m0, m_len, vu);
-  pair_emit_chunk(pa, stg, issued, lane, col0, m0, m_len, va);
+  pair_emit_chunk<NBUF>(pg, stg, issued, lane, col0, m0, m_len, vg);
+  pair_emit_chunk<NBUF>(pu, stg, issued, lane, col0, m0, m_len, vu);
+  pair_emit_chunk<NBUF>(pa, stg, issued, lane, col0, m0, m_len, va);
 }
 
 template <bool B_MN, int NB, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
     plora_gemm_pair_kernel(const __grid_constant__ PairArgs p) {
-  using Cfg = PairCfg<NB>;
+  using Cfg = PairCfg<NB, EPI>;
   const GemmArgs& args = p.g;
   constexpr int S = Cfg::kStages;
   constexpr int AS = Cfg::kAccStages;
@@ -836,7 +841,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     constexpr int kDirect = Cfg::kAccStages > 1 ? kChunks : 3;
     constexpr int kParked = kChunks - kDirect;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
-    uint8_t* stg = smem + S * Cfg::kStageBytes + 1024 + ew * 4096;   // 1024-B aligned (>= swizzle period)
+    uint8_t* stg = smem + S * Cfg::kStageBytes + 1024 + ew * (Cfg::kStgBufs * 2048);   // 1024-B aligned
     int acc = 0;
     uint32_t acc_phase = 0;
     int issued = 0;
@@ -876,7 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
 #pragma unroll
           for (int q = 0; q < 16; ++q) vu[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
           if (i < kDirectPairs) {
-            if (store) pair_emit_swiglu(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len, vg, vu);
+            if (store) pair_emit_swiglu<Cfg::kStgBufs>(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len, vg, vu);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -892,7 +897,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
         if (!store) continue;
 #pragma unroll
         for (int i = kDirectPairs; i < kPairs; ++i)
-          pair_emit_swiglu(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len,
+          pair_emit_swiglu<Cfg::kStgBufs>(pg, pu, pa, stg, issued, lane, t.n0 + (chalf * 4 + i) * 32, m0, m_len,
                            kg[i - kDirectPairs], ku[i - kDirectPairs]);
       }
     } else

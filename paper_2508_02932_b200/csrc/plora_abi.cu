@@ -180,12 +180,12 @@ template <bool B_MN, int NB, int EPI = EPI_STORE>
 static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   auto kern = plora_gemm_pair_kernel<B_MN, NB, EPI>;
   static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
-  if (ensure_smem(kern, PairCfg<NB>::kSmemBytes, configured)) return 1;
+  if (ensure_smem(kern, PairCfg<NB, EPI>::kSmemBytes, configured)) return 1;
   const int total = args.g.n_groups * args.g.n_ntiles;
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
   const int clusters = total < max_clusters ? total : max_clusters;
-  kern<<<clusters * 2, PairCfg<NB>::kThreads, PairCfg<NB>::kSmemBytes, stream>>>(args);
+  kern<<<clusters * 2, PairCfg<NB, EPI>::kThreads, PairCfg<NB, EPI>::kSmemBytes, stream>>>(args);
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
