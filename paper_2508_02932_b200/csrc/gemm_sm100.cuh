@@ -848,7 +848,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     if constexpr (EPI == EPI_SWIGLU) {
       // paired gate/up tile: warp (quarter, chalf) owns gate chunks chalf*4+i (TMEM cols
       // 0..255) and the matching up chunks 8+chalf*4+i; per pair it stores g, u and act.
-      constexpr int kPairs = 4, kDirectPairs = 3;
+      constexpr int kPairs = 4, kDirectPairs = 2;
       for (int idx = cluster; idx < total; idx += n_clusters) {
         const PairTile t = decode_pair_tile<NB>(p, idx);
         const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;
