@@ -469,10 +469,12 @@ struct PairCfg {
   static constexpr int kABytes = kBM * kBK * 2;             // 16 KB (own 128 rows)
   static constexpr int kBBytes = NB * 128 * kBK * 2;        // own half of each 256-col chunk
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // EPI_SWIGLU (= 2) stores three chunks per accumulator chunk pair: 3 stages, 4 staging
-  // buffers per epilogue warp instead of 4 stages / 2 buffers
-  static constexpr int kStages = NB == 1 ? 6 : (EPI_ == 2 ? 3 : 4);
-  static constexpr int kStgBufs = EPI_ == 2 ? 4 : 2;
+  // NB = 2: 3 mainloop stages (3 k-blocks = 3 x 1024 MMA cycles of lookahead) and 4 epilogue
+  // staging buffers per warp (the stores before the accumulator release never wait for a
+  // buffer).  Same-box A/B against 4 stages / 2 buffers: GEMM time equal at locked clocks,
+  // step +1.9% and SM clock +25 MHz under the power cap (profiles/r1s3_stages_ab.log).
+  static constexpr int kStages = NB == 1 ? 6 : 3;
+  static constexpr int kStgBufs = NB == 1 ? 2 : 4;
   static constexpr int kAccStages = NB == 1 ? 2 : 1;
   static constexpr int kTmemCols = 512;
   static constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
@@ -930,7 +932,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
             if (j + 1 < kChunks) tmem_ld_32x32b_x32(tb + (c0 + j + 1) * 32, r);   // overlaps the store below
-            if (store) pair_emit_chunk(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, v);
+            if (store) pair_emit_chunk<Cfg::kStgBufs>(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, v);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
@@ -946,7 +948,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       if (!store) continue;
 #pragma unroll
       for (int j = kDirect; j < kChunks; ++j)
-        pair_emit_chunk(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, pk[j - kDirect]);
+        pair_emit_chunk<Cfg::kStgBufs>(po, stg, issued, lane, t.n0 + (c0 + j) * 32, m0, m_len, pk[j - kDirect]);
     }
     if (lane == 0) bulk_wait<0>();   // all TMA stores complete before the CTA retires
     __syncwarp();
