@@ -463,6 +463,16 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 // CTAs' empty / tmem_full barriers; both CTAs' epilogues drain their own 128 TMEM
 // lanes and arrive on the leader's tmem_empty barrier.  Pair tiles never straddle
 // adapters (meta builder), so the fused LoRA K-steps use one adapter's B_i.
+#ifndef PLORA_PAIR_STAGES
+#define PLORA_PAIR_STAGES 3   // NB = 2 mainloop stages (build-time knob for experiments)
+#endif
+#ifndef PLORA_PAIR_BUFS
+#define PLORA_PAIR_BUFS 4     // NB = 2 epilogue staging buffers per warp
+#endif
+#ifndef PLORA_PAIR_KDIRECT
+#define PLORA_PAIR_KDIRECT 4  // NB = 2 chunks stored before the accumulator release (rest parked)
+#endif
+
 template <int NB, int EPI_ = 0>
 struct PairCfg {
   static constexpr int kBN = 256 * NB;                      // output columns per pair tile
@@ -470,11 +480,12 @@ struct PairCfg {
   static constexpr int kBBytes = NB * 128 * kBK * 2;        // own half of each 256-col chunk
   static constexpr int kStageBytes = kABytes + kBBytes;
   // NB = 2: 3 mainloop stages (3 k-blocks = 3 x 1024 MMA cycles of lookahead) and 4 epilogue
-  // staging buffers per warp (the stores before the accumulator release never wait for a
-  // buffer).  Same-box A/B against 4 stages / 2 buffers: GEMM time equal at locked clocks,
-  // step +1.9% and SM clock +25 MHz under the power cap (profiles/r1s3_stages_ab.log).
-  static constexpr int kStages = NB == 1 ? 6 : 3;
-  static constexpr int kStgBufs = NB == 1 ? 2 : 4;
+  // staging buffers per warp, 4 chunks stored before the accumulator release (4 parked: no
+  // spills).  Same-box A/B against 4 stages / 2 buffers / 3 direct: GEMM time equal at locked
+  // clocks, step +1.9% (stages) and +0.5% (kDirect) with the SM clock higher under the power
+  // cap; 2 stages starve the MMA (-14%) (profiles/r1s3_stages_ab.log).
+  static constexpr int kStages = NB == 1 ? 6 : PLORA_PAIR_STAGES;
+  static constexpr int kStgBufs = NB == 1 ? 2 : PLORA_PAIR_BUFS;
   static constexpr int kAccStages = NB == 1 ? 2 : 1;
   static constexpr int kTmemCols = 512;
   static constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quarter
@@ -840,7 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     constexpr int kChunks = Cfg::kBN / 32 / 2;   // chunks per warp
     // chunks stored before the accumulator is released: all of them when the accumulator is
     // double-buffered (NB = 1), otherwise park the rest in registers
-    constexpr int kDirect = Cfg::kAccStages > 1 ? kChunks : 3;
+    constexpr int kDirect = Cfg::kAccStages > 1 ? kChunks : PLORA_PAIR_KDIRECT;
     constexpr int kParked = kChunks - kDirect;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint8_t* stg = smem + S * Cfg::kStageBytes + 1024 + ew * (Cfg::kStgBufs * 2048);   // 1024-B aligned
