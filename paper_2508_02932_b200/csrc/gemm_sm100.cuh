@@ -66,12 +66,23 @@ constexpr int kBK = 64;
 constexpr int kThreads = 192;
 constexpr int kBand = 16;  // row groups per raster band (L2 reuse of the B operand)
 
+#ifndef PLORA_G64_STAGES
+#define PLORA_G64_STAGES 8    // 1-CTA kernel stages at BN = 64 / 128 / 192 (build-time knobs)
+#endif
+#ifndef PLORA_G128_STAGES
+#define PLORA_G128_STAGES 6
+#endif
+#ifndef PLORA_G192_STAGES
+#define PLORA_G192_STAGES 5
+#endif
+
 template <int BN>
 struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;              // 16 KB
   static constexpr int kBBytes = BN * kBK * 2;               // BN x 64 bf16
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN == 256) ? 4 : (BN == 192 ? 5 : (BN == 128 ? 6 : 8));
+  static constexpr int kStages = (BN == 256) ? 4 : (BN == 192 ? PLORA_G192_STAGES : (BN == 128 ? PLORA_G128_STAGES :
+                                                                                     PLORA_G64_STAGES));
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 :
                                    (2 * BN <= 256 ? 256 : 512)));   // power of two >= 2 accumulators
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
