@@ -69,6 +69,10 @@ static EncodeTiledFn get_encode() {
 }
 
 // 2D bf16 tensor [outer][inner] with row pitch `pitch_elems`, 128B-swizzled boxes.
+#ifndef PLORA_LOAD_L2_PROMOTION
+#define PLORA_LOAD_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B   // operand loads (build-time knob)
+#endif
+
 static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn enc = get_encode();
@@ -82,7 +86,7 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   PLORA_LOAD_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail("cuTensorMapEncodeTiled(2d inner=%llu outer=%llu box=%u,%u) failed: %d",
                 (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer, (int)r);
@@ -118,7 +122,7 @@ static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   PLORA_LOAD_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled(3d) failed: %d", (int)r);
   return 0;
 }
