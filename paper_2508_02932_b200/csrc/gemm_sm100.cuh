@@ -24,6 +24,16 @@
 
 namespace plora {
 
+#ifndef PLORA_EPI_SUSPEND_NS
+#define PLORA_EPI_SUSPEND_NS 0   // epilogue accumulator wait: 0 = poll, else try_wait suspend hint (ns)
+#endif
+#if PLORA_EPI_SUSPEND_NS > 0
+#define PLORA_EPI_WAIT(bar, par) mbar_wait_suspend(bar, par, PLORA_EPI_SUSPEND_NS)
+#else
+#define PLORA_EPI_WAIT(bar, par) mbar_wait(bar, par)
+#endif
+
+
 enum GemmMode : int { MODE_GEMM = 0, MODE_SHRINK = 1, MODE_SEGRED = 2 };
 
 struct __align__(64) GemmArgs {
@@ -350,7 +360,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
           }
           continue;
         }
-        mbar_wait(&tfull_bar[acc], acc_phase);
+        PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
@@ -372,7 +382,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
         }
       } else {
         if (nblk == 0) continue;
-        mbar_wait(&tfull_bar[acc], acc_phase);
+        PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
         const float scale = (MODE == MODE_SHRINK) ? args.alpha[t.adapter] : 1.0f;
@@ -877,7 +887,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
         const PairTile t = decode_pair_tile<NB>(p, idx);
         const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;
         const int m_len = min(32, t.m_len - static_cast<int>(rank) * 128 - quarter * 32);
-        mbar_wait(&tfull_bar[acc], acc_phase);
+        PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
         const bool store = m_len > 0;
@@ -929,7 +939,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       const PairTile t = decode_pair_tile<NB>(p, idx);
       const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;   // this warp's 32 rows
       const int m_len = min(32, t.m_len - static_cast<int>(rank) * 128 - quarter * 32);
-      mbar_wait(&tfull_bar[acc], acc_phase);
+      PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
       const int c0 = chalf * kChunks;
