@@ -248,7 +248,7 @@ class PackedLoraTrainer:
                                 a_scale=a_scale, b_std=b_std, full_targets=cfg.targets(),
                                 shard=self.shard if self.tp is not None else None)
         self.cos, self.sin = rope_tables(cfg, seq_len, self.device)
-        self.ce_chunk = ce_chunk
+        self.ce_chunk = int(os.environ.get("PLORA_CE_CHUNK", ce_chunk))   # tokens per lm_head + CE chunk
         # per-token adapter id and the CE weight 1/n_i (labels exist for s-1 tokens per sequence)
         ta = torch.from_numpy(self.meta.token_adapter.astype("int64")).to(self.device)
         n_lab = torch.tensor([max(sp.batch * (seq_len - 1), 1) for sp in specs], dtype=torch.float32,
