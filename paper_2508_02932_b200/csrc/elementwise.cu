@@ -429,12 +429,16 @@ __global__ void add_row_bias_kernel(bf16* __restrict__ y, const bf16* __restrict
   }
 }
 
+#ifndef PLORA_EW_BLOCKS_PER_SM
+#define PLORA_EW_BLOCKS_PER_SM 16   // grid-stride elementwise kernels: resident blocks per SM (build-time knob)
+#endif
+
 int grid_for(int64_t n, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (n + threads - 1) / threads;
-  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  const int64_t cap = static_cast<int64_t>(sms) * PLORA_EW_BLOCKS_PER_SM;
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
