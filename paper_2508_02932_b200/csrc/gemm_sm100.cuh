@@ -487,6 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 #ifndef PLORA_PAIR_STAGES
 #define PLORA_PAIR_STAGES 3   // NB = 2 mainloop stages (build-time knob for experiments)
 #endif
+#ifndef PLORA_PAIR_NB1_STAGES
+#define PLORA_PAIR_NB1_STAGES 6   // NB = 1 (256 x 256, K <= 1024) mainloop stages
+#endif
 #ifndef PLORA_PAIR_BUFS
 #define PLORA_PAIR_BUFS 4     // NB = 2 epilogue staging buffers per warp
 #endif
@@ -505,7 +508,7 @@ struct PairCfg {
   // spills).  Same-box A/B against 4 stages / 2 buffers / 3 direct: GEMM time equal at locked
   // clocks, step +1.9% (stages) and +0.5% (kDirect) with the SM clock higher under the power
   // cap; 2 stages starve the MMA (-14%) (profiles/r1s3_stages_ab.log).
-  static constexpr int kStages = NB == 1 ? 6 : PLORA_PAIR_STAGES;
+  static constexpr int kStages = NB == 1 ? PLORA_PAIR_NB1_STAGES : PLORA_PAIR_STAGES;
   static constexpr int kStgBufs = NB == 1 ? 2 : PLORA_PAIR_BUFS;
   static constexpr int kAccStages = NB == 1 ? 2 : 1;
   static constexpr int kTmemCols = 512;
