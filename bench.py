@@ -1,19 +1,27 @@
 """Packed multi-LoRA training throughput (tokens/s, summed over adapters) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama-3.1-8b] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama-3.1-8b]
+                    [--scaling split|weak] [--impl ours|reference]
 
 Workload (BASELINE.json configs[2]): Llama-3.1-8B shapes,
 random-init frozen bf16 base, 16 packed LoRA adapters on all 7 targets (ranks
 8/16/32/64 x4, raw alpha = r*{0.25,1,2,4}, b_i in {1,2,4} sequences of 1024 tokens,
-T = 32768 tokens/step/GPU), synthetic uniform tokens.  One step = forward +
-backward + fused per-adapter AdamW.  Multi-GPU: one process per GPU, each rank
-trains its own independent packed job (the planner's job-level parallelism; no
-data-path collective) -> "scaling": "weak".
+T = 32768 tokens/step), synthetic uniform tokens.  One step = forward + backward +
+fused per-adapter AdamW.
 
---impl reference times the reference algorithm (the oracle port of
-lorasweep.packed_forward/packed_backward, numpy fp64, all host cores) on a bounded
-sample of the same workload (the 7 LoRA linears of one layer at 1/16 of the tokens,
-scaled linearly to the full model and step).
+Multi-GPU (one process per GPU; ``--gpus N`` outside torchrun starts the N ranks
+itself): by default the planner splits the workload's adapters over the N GPUs
+(sweep/jobsplit.py: ``plan_split`` + ``place``, BASELINE configs[2] "via planner"),
+so rank r trains the packed job placed on device r -- independent jobs, no data-path
+collective, fixed total work ("scaling": "strong"); ``--scaling weak`` replicates the
+whole workload on every GPU.  ``--config qwen2.5-32b`` (C4) runs one tensor-parallel
+job over all GPUs (tp.py, NCCL).  value = tokens of all ranks / the max over ranks of
+the device-timed region.
+
+--impl reference times the reference's own CPU implementation (lorasweep from
+baseline/_ref: pack_adapters + packed_forward + packed_backward, numpy fp64, all host
+cores) on a bounded sample of the same workload (the 7 LoRA linears of one layer at
+1/16 of the tokens, scaled linearly to the full model and step).
 """
 
 from __future__ import annotations
@@ -97,22 +105,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(cfg_name: str, frac: float | None = None) -> dict:
-    """Reference CPU path (oracle port of lorasweep.packed_forward/backward, fp64
-    numpy/OpenBLAS on all host cores) over the 7 LoRA linears of ONE layer at a
-    fraction f of the step's tokens; throughput scaled by 1/(L) (cost linear in T)."""
+def _ref_lorapack():
+    """The reference's own lorapack (lorasweep installed into baseline/_ref, git-ignored,
+    travels to the box) -- or None when it is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "lorasweep" / "lorapack.py").exists() and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import lorasweep.lorapack as RL   # noqa: N812
+    except ImportError:
+        return None
+    return RL
+
+
+def _cpu_sample(cfg_name: str, frac: float | None):
+    """The bounded CPU sample of one training step: the 7 LoRA linears of ONE layer at a
+    fraction f of the step's tokens (fp64, seeded)."""
     import numpy as np
 
-    from oracle import lorapack_oracle as O
     from paper_2508_02932_b200.model import PRESETS, bench_adapters
 
     cfg = PRESETS[cfg_name]
     specs, s = bench_adapters(cfg_name)
     if frac is None:
-        frac = {"tiny": 1.0, "qwen2.5-3b": 1 / 8, "llama-3.1-8b": 1 / 16, "qwen2.5-32b": 1 / 32}[cfg_name]
+        frac = {"tiny": 1.0, "tiny-qwen": 1.0, "qwen2.5-3b": 1 / 8, "llama-3.1-8b": 1 / 16,
+                "qwen2.5-32b": 1 / 32}[cfg_name]
     rng = np.random.default_rng(0)
     toks = [max(1, int(sp.batch * s * frac)) for sp in specs]
-    T = sum(toks)
     work = []
     for t in cfg.targets():
         downs = [rng.uniform(-1, 1, (t.h_in, sp.rank)) / np.sqrt(t.h_in) for sp in specs]
@@ -120,26 +139,89 @@ def cpu_reference(cfg_name: str, frac: float | None = None) -> dict:
         xs = [rng.standard_normal((n, t.h_in)) for n in toks]
         dys = [rng.standard_normal((n, t.h_out)) for n in toks]
         w = rng.standard_normal((t.h_in, t.h_out)) * 0.02
-        work.append((O.pack(downs, ups, [sp.alpha for sp in specs], xs), w, dys))
-    # warm the BLAS threads on a small problem, then time the layer once
-    O.packed_backward(*work[0][:2], work[0][2]) if T <= 4096 else O.packed_forward(work[0][0], work[0][1])
-    t0 = time.perf_counter()
-    for p, w, dys in work:
-        O.packed_forward(p, w)
-        O.packed_backward(p, w, dys)
-    dt = time.perf_counter() - t0
+        work.append((downs, ups, [float(sp.alpha) for sp in specs], xs, w, dys))
+    return cfg, specs, s, frac, toks, work
+
+
+def _all_host_threads() -> None:
+    """torchrun exports OMP_NUM_THREADS=1; the CPU reference uses every host core."""
+    try:
+        import numpy  # noqa: F401  (load OpenBLAS first: threadpoolctl only sees loaded libraries)
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
+    except Exception:  # pragma: no cover
+        pass
+
+
+def _blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
-        blas = max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+        return int(max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"),
+                       default=1))
     except Exception:  # pragma: no cover
-        blas = os.cpu_count() or 1
-    tok_s = T / (dt * cfg.n_layers)
-    return {"value": tok_s, "unit": "tokens/s", "cores": int(blas), "kind": "port",
-            "sample": (f"oracle port of lorasweep packed_forward+packed_backward (fp64 numpy, {blas} BLAS threads), "
-                       f"7 LoRA linears of 1 of {cfg.n_layers} layers at {T} tokens (1/{round(1 / frac)} of the "
-                       f"{sum(sp.batch for sp in specs) * s}-token step), {dt:.2f} s, scaled by 1/L; attention, norms, "
-                       f"lm_head and optimizer excluded (the reference implements none)"),
-            "host_cpus": os.cpu_count()}
+        return os.cpu_count() or 1
+
+
+class CpuReference:
+    """The reference CPU path of one step, as a bounded sample: lorasweep's own
+    ``pack_adapters`` -> ``packed_forward`` -> ``packed_backward`` (pkg/src/lorasweep/
+    lorapack.py:128-231, fp64 numpy/OpenBLAS on every host core) over the 7 LoRA linears
+    of one layer at 1/16 (C3) of the step's tokens; tokens/s are scaled by 1/L (the cost
+    is linear in T and in the layer count).  Uses the real reference from baseline/_ref
+    ("kind": "reference"); without it, the oracle port (oracle/lorapack_oracle.py,
+    "kind": "port")."""
+
+    def __init__(self, cfg_name: str, frac: float | None = None):
+        self.cfg, self.specs, self.s, self.frac, toks, work = _cpu_sample(cfg_name, frac)
+        self.T = sum(toks)
+        self.RL = _ref_lorapack()
+        if self.RL is not None:
+            RL = self.RL
+            self.kind = "reference"
+            self.work = [([RL.AdapterWeights(a, b, al) for a, b, al in zip(downs, ups, alphas)], xs, w, dys)
+                         for downs, ups, alphas, xs, w, dys in work]
+        else:
+            from oracle import lorapack_oracle as O
+            self.kind = "port"
+            self.O = O
+            self.work = [(O.pack(downs, ups, alphas, xs), w, dys) for downs, ups, alphas, xs, w, dys in work]
+
+    def step(self) -> float:
+        """One sample step; returns its wall seconds."""
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            RL = self.RL
+            for ads, xs, w, dys in self.work:
+                packed = RL.pack_adapters(ads, xs)
+                RL.packed_forward(packed, w)
+                RL.packed_backward(packed, w, dys)
+        else:
+            for p, w, dys in self.work:
+                self.O.packed_forward(p, w)
+                self.O.packed_backward(p, w, dys)
+        return time.perf_counter() - t0
+
+    def tok_s(self, dt: float) -> float:
+        return self.T / (dt * self.cfg.n_layers)
+
+    def describe(self, dt: float) -> str:
+        what = ("lorasweep (the reference, baseline/_ref) pack_adapters+packed_forward+packed_backward"
+                if self.kind == "reference" else "oracle port of lorasweep packed_forward+packed_backward")
+        step_tokens = sum(sp.batch for sp in self.specs) * self.s
+        return (f"{what} (fp64 numpy, {_blas_threads()} BLAS threads), 7 LoRA linears of 1 of {self.cfg.n_layers} "
+                f"layers at {self.T} tokens (1/{round(1 / self.frac)} of the {step_tokens}-token step), "
+                f"{dt:.2f} s per sample, scaled by 1/L; attention, norms, lm_head and optimizer excluded "
+                f"(the reference implements none)")
+
+
+def cpu_reference(cfg_name: str, frac: float | None = None) -> dict:
+    """cpu_baseline: one warm-up sample, then the best of two timed samples."""
+    _all_host_threads()
+    ref = CpuReference(cfg_name, frac)
+    ref.step()
+    dt = min(ref.step(), ref.step())
+    return {"value": ref.tok_s(dt), "unit": "tokens/s", "cores": _blas_threads(), "kind": ref.kind,
+            "sample": ref.describe(dt), "host_cpus": os.cpu_count()}
 
 
 def dropin_api_sample(cfg_name: str) -> dict:
@@ -184,33 +266,68 @@ def dropin_api_sample(cfg_name: str) -> dict:
 
 
 def run_reference(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's CPU implementation of the path (module doc).
+    Each step is one bounded sample (one layer's 7 LoRA linears at 1/16 of the tokens),
+    so ms_per_step is the sample's measured time; value is the tokens/s of the whole
+    model that the sample implies (x 1/L).  Under torchrun only rank 0 runs."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    base = cpu_reference(args.config)
-    from paper_2508_02932_b200.model import PRESETS, bench_adapters
-    specs, s = bench_adapters(args.config)
-    T = sum(sp.batch for sp in specs) * s
-    # per step: the sampled layer's work, scaled; --steps/--warmup bound the run
-    vals = [base["value"]]
-    for _ in range(max(0, args.steps - 1)):
-        if time.perf_counter() - _T0 > 120:
+    _all_host_threads()
+    ref = CpuReference(args.config)
+    for _ in range(args.warmup):
+        ref.step()
+    dts = []
+    for _ in range(max(1, args.steps)):
+        dts.append(ref.step())
+        if time.perf_counter() - _T0 > 240:   # keep the arm within a few minutes
             break
-        vals.append(cpu_reference(args.config)["value"])
-    v = statistics.median(vals)
-    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(vals),
-            "warmup": args.warmup, "ms_per_step": 1000.0 * T / v, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"{PRESETS[args.config].name} packed LoRA, {len(specs)} adapters, T={T}",
-                       "model": PRESETS[args.config].name, "global_batch": T // s, "seq_len": s,
-                       "parallelism": "cpu"},
-            "cpu_baseline": {**base, "value": v},
+    dt = sum(dts) / len(dts)
+    v = ref.tok_s(dt)
+    s = ref.s
+    T = sum(sp.batch for sp in ref.specs) * s
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(dts),
+            "warmup": args.warmup, "ms_per_step": 1000.0 * dt, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{ref.cfg.name} packed LoRA, {len(ref.specs)} adapters, T={T}",
+                       "model": ref.cfg.name, "global_batch": T // s, "seq_len": s, "parallelism": "cpu",
+                       "step": f"one bounded sample: 7 LoRA linears of 1 layer at {ref.T} tokens"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": _blas_threads(), "kind": ref.kind,
+                             "sample": ref.describe(dt), "host_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 _T0 = time.perf_counter()
+
+
+def _relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks (one process per GPU) on this node
+    through torch.distributed.run, exactly as the driver does, and pass rank 0's line
+    through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def job_for_rank(cfg_name: str, world: int, rank: int, scaling: str) -> tuple[list, list, str]:
+    """(bench-adapter indices, all-adapter count, parallelism tag) of this rank's packed job.
+    split (default): the planner's one-batch split of the workload over the world
+    (sweep/jobsplit.py: plan_split + place), so rank r trains the job placed on device r;
+    weak: every rank trains the whole workload (independent replicas)."""
+    from paper_2508_02932_b200.model import bench_adapters
+
+    n = len(bench_adapters(cfg_name)[0])
+    if world == 1 or scaling == "weak":
+        return list(range(n)), n, f"jobs{world}" if world > 1 else "jobs1"
+    from paper_2508_02932_b200.sweep.jobsplit import split_adapters
+
+    sp = split_adapters(cfg_name, world)
+    return list(sp.adapters[rank]), n, sp.describe()
 
 
 def main() -> None:
@@ -220,6 +337,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="llama-3.1-8b")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="split", choices=["split", "weak"],
+                    help="split: the planner splits the workload's adapters over the GPUs (one packed job "
+                         "per GPU, fixed total work); weak: every GPU trains the whole workload")
     ap.add_argument("--tp", type=int, default=None,
                     help="tensor-parallel degree per packed job (config C4 default: all GPUs); "
                          "world/tp independent jobs run side by side")
@@ -227,6 +347,11 @@ def main() -> None:
                     help="TP all-reduce through torch.distributed (NCCL) or libplora's C-ABI (plora_tp_*, NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(_relaunch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -237,15 +362,20 @@ def main() -> None:
 
     from paper_2508_02932_b200 import _lib, ops
     from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
-
     from paper_2508_02932_b200.tp import AbiNcclComm, DistComm
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    device = local % max(1, ndev)
+    shared = world > ndev          # several ranks on one GPU (test runs): NCCL refuses that
+    torch.cuda.set_device(device)
+    backend = "gloo" if shared else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
     _lib.check(_lib.lib().plora_device_check(), "device check")
 
     cfg = PRESETS[args.config]
@@ -255,37 +385,64 @@ def main() -> None:
     if args.config == "qwen2.5-32b" and tp < 8:
         raise SystemExit("C4 (Qwen2.5-32B, 32 adapters) needs a tensor-parallel group of 8 GPUs "
                          "(one 180 GB B200 holds a TP=8 shard: tools/c4_shard_bench.py)")
+    if tp > 1 and shared:
+        raise SystemExit("tensor-parallel jobs need one GPU per rank")
     n_jobs = world // tp
     job = rank // tp
     comm = None
+    all_specs, s = bench_adapters(args.config)
     if tp > 1:   # one NCCL group per packed job (Megatron TP over NVLink), jobs side by side
         groups = [dist.new_group(list(range(j * tp, (j + 1) * tp))) for j in range(n_jobs)]
         if args.tp_comm == "abi":
             comm = AbiNcclComm(rank - job * tp, tp, group=groups[job])
         else:
             comm = DistComm(groups[job])
-    specs, s = bench_adapters(args.config)
-    n = len(specs)
-    trainer = PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=[100 + i + 1000 * job for i in range(n)],
-                                tp=comm)
-    T = trainer.T
-    tokens_host = trainer.synthetic_tokens(seed_base=1000 + 100000 * job).pin_memory()
-    tokens = tokens_host.to("cuda")
+        mine, parallelism = list(range(len(all_specs))), f"jobs{n_jobs}xtp{tp}"
+        scaling = "weak" if args.tp is not None else "strong"
+        seed_off = 1000 * job
+    else:
+        mine, _, parallelism = job_for_rank(args.config, world, rank, args.scaling)
+        scaling = "weak" if (args.scaling == "weak" or world == 1) else "strong"
+        seed_off = 1000 * rank if args.scaling == "weak" else 0
+    specs = [all_specs[i] for i in mine]
+    trainer = None
+    T = 0
+    if specs:
+        trainer = PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=[100 + i + seed_off for i in mine],
+                                    tp=comm)
+        T = trainer.T
+        tokens_host = trainer.synthetic_tokens(seeds=[1000 + i + 100 * seed_off for i in mine]).pin_memory()
+        tokens = tokens_host.to("cuda")
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     for _ in range(args.warmup):
-        trainer.step(tokens)
+        if trainer is not None:
+            trainer.step(tokens)
     barrier()
 
     # ---------------------------------------------------------------- timed region (device)
     timer = ops.KernelTimer()
     launches0 = ops.launch_count()
     profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
-    with ClockSampler(local) as clocks:
+    with ClockSampler(device) as clocks:
         barrier()
         if profile_range:
             torch.cuda.profiler.start()
@@ -294,7 +451,8 @@ def main() -> None:
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            trainer.step(tokens)
+            if trainer is not None:
+                trainer.step(tokens)
         e1.record()
         ops.set_timer(None)
         barrier()
@@ -303,43 +461,31 @@ def main() -> None:
     launches = ops.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     kstats = timer.summary()
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    value = n_jobs * T * args.steps / (ms_max / 1000.0)
-    losses_dev = trainer.losses.clone()
+    ms_max = max_over_ranks(ms)
+    # tokens processed by the whole job: a TP group's ranks share one job's tokens
+    tokens_all = sum_over_ranks(float(T) if (tp == 1 or rank % tp == 0) else 0.0)
+    value = tokens_all * args.steps / (ms_max / 1000.0)
+    losses_dev = trainer.losses.clone() if trainer is not None else torch.zeros(0)
 
     # ---------------------------------------------------------------- end-to-end (public API, host buffers)
     barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record()
+    losses_host = torch.zeros(0)
     for _ in range(args.steps):
-        tokens.copy_(tokens_host, non_blocking=True)
-        losses_host = trainer.step(tokens).cpu()
+        if trainer is not None:
+            tokens.copy_(tokens_host, non_blocking=True)
+            losses_host = trainer.step(tokens).cpu()
     e3.record()
     barrier()
-    ms_e2e = e2.elapsed_time(e3)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    e2e_value = n_jobs * T * args.steps / (ms_e2e / 1000.0)
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
+    e2e_value = tokens_all * args.steps / (ms_e2e / 1000.0)
 
     peaks = _peaks()
     g = kstats.get("gemm", {"ms": 0.0, "flops": 0.0, "launches": 0})
     achieved = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g["ms"] else 0.0
-    traffic = None
-    prof = ROOT / "profiles" / "gemm_traffic.json"
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    kernels = {}
-    shapes = {}
+    kernels, shapes = {}, {}
     for kind, d in kstats.items():
         sec = d["ms"] / 1000.0
         if "[" in kind:   # per-shape GEMM detail
@@ -347,38 +493,56 @@ def main() -> None:
                                                    "tflops": round(d["flops"] / sec / 1e12, 1)}
             continue
         kernels[kind] = {"launches": d["launches"], "ms_total": round(d["ms"], 3),
-                         "share_of_step": round(d["ms"] / ms, 4)}
+                         "share_of_step": round(d["ms"] / ms, 4) if ms else 0.0}
         if d["flops"]:
             kernels[kind]["tflops"] = round(d["flops"] / sec / 1e12, 1)
         if d["bytes"]:
             kernels[kind]["hbm_gbs"] = round(d["bytes"] / sec / 1e9, 1)
             kernels[kind]["hbm_frac"] = round(d["bytes"] / sec / 1e9 / peaks["hbm_gbs"], 3)
-    base_tf = value / world * cfg.base_flops_per_token() / 1e12   # per GPU
+    step_s = ms_max / 1000.0 / args.steps
+    useful = useful_flops(cfg, specs, s, tp) if specs else {"base": 0.0, "lora": 0.0, "attention": 0.0}
+    useful_all = {k: sum_over_ranks(v) for k, v in useful.items()}   # this rank's share, summed
+    per_rank = {"rank": rank, "device": device, "world": dist.get_world_size() if world > 1 else 1,
+                "backend": backend if world > 1 else None, "adapters": mine, "tokens": T,
+                "ms_per_step": round(ms / args.steps, 2),
+                "tokens_per_s": round(T * args.steps / (ms / 1000.0), 1) if ms and T else 0.0,
+                "gemm_tflops": round(achieved, 1), "gemm_frac": round(achieved / peaks["tflops_sustained"], 4),
+                "step_base_tflops": round(useful["base"] * args.steps / (ms / 1000.0) / 1e12, 1) if ms else 0.0}
+    ranks = [per_rank]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, per_rank)
+    base_tf = sum(r["step_base_tflops"] for r in ranks) / len(ranks)   # per GPU
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak" if args.tp is not None or tp == 1 else "strong",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
-        "config": {"workload": f"{cfg.name} packed LoRA training, {n} adapters (ranks 8/16/32/64), all 7 targets, "
-                               f"T={T} tokens/step/GPU, fwd+bwd+per-adapter AdamW",
-                   "model": cfg.name, "global_batch": n_jobs * T // s, "seq_len": s,
-                   "parallelism": f"jobs{n_jobs}" + (f"xtp{tp}" if tp > 1 else ""),
-                   "adapters": n, "l2": "working set (~100 GB activations) >> 126 MB L2; no flush needed"},
+        "scaling": scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
+        "config": {"workload": f"{cfg.name} packed LoRA training, {len(all_specs)} adapters (ranks 8/16/32/64), "
+                               f"all 7 targets, {sum(sp.batch for sp in all_specs) * s} tokens/step per job, "
+                               f"fwd+bwd+per-adapter AdamW",
+                   "model": cfg.name, "global_batch": int(tokens_all) // s, "seq_len": s,
+                   "parallelism": parallelism, "adapters": len(all_specs),
+                   "l2": "working set (~100 GB activations) >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 base GEMM + fused LoRA expand (K1/K2b/K6, lm_head)",
                      "achieved": round(achieved, 1), "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": round(achieved / peaks["tflops_sustained"], 4), "traffic": traffic,
+                     "frac": round(achieved / peaks["tflops_sustained"], 4), "traffic": _traffic(),
                      "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside a long step)",
                      "step_base_gemm_tflops": round(base_tf, 1),
                      "step_frac_of_burst_peak": round(base_tf / peaks["tflops_burst"], 4)},
+        "useful_tflops_per_gpu": {k: round(v * args.steps / (ms_max / 1000.0) / 1e12 / world, 1)
+                                  for k, v in useful_all.items()},
         "kernels": kernels,
         "gemm_shapes": shapes,
-        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": tokens_host.numel() * tokens_host.element_size(),
+        "e2e": {"value": e2e_value, "unit": "tokens/s",
+                "h2d_bytes_per_step": (tokens_host.numel() * tokens_host.element_size()) if trainer is not None else 0,
                 "d2h_bytes_per_step": losses_host.numel() * losses_host.element_size()},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "losses": [round(float(x), 4) for x in losses_dev.tolist()],
         "mem_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
     }
+    if world > 1:
+        line["ranks"] = ranks
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(args.config)
         line["dropin_api"] = dropin_api_sample(args.config)
@@ -386,6 +550,33 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def useful_flops(cfg, specs, s: int, tp: int = 1) -> dict:
+    """Useful FLOPs of one step of a packed job, this rank's share (1/tp of the job):
+    base = 4 (sum_layers sum_targets h_in h_out + d V) per token (forward X W + backward
+    dY W^T; the frozen base has no dW); lora = 6 r_i sum(h_in +
+    h_out) L per token of adapter i (reference lora_flop, costmodel.py:168-178);
+    attention = causal SDPA, 2 forward + 4 backward matmuls of 2 s^2 hd / 2 per head,
+    sequence and layer."""
+    T = sum(sp.batch for sp in specs) * s
+    base = cfg.base_flops_per_token() * T
+    lora = cfg.lora_flops_per_token_per_rank() * sum(sp.rank * sp.batch * s for sp in specs)
+    seqs = sum(sp.batch for sp in specs)
+    attn = 6 * 2.0 * s * s * cfg.head_dim / 2 * cfg.n_heads * seqs * cfg.n_layers
+    return {"base": base / tp, "lora": lora / tp, "attention": attn / tp}   # one rank's share
+
+
+def _traffic():
+    """ncu DRAM bytes per launch of the dominant GEMM launch of the timed step
+    (profiles/gemm_traffic.json, written from the step's own ncu capture)."""
+    prof = ROOT / "profiles" / "gemm_traffic.json"
+    if not prof.exists():
+        return None
+    try:
+        return json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 if __name__ == "__main__":

@@ -80,7 +80,10 @@ class PackedAdapters:
     alphas: tuple
     rank_offsets: tuple
     row_offsets: tuple
-    _meta: list = field(default_factory=list, repr=False, compare=False)
+    # device segment index, built once per instance (init=False: ``dataclasses.replace``
+    # gives the new instance an empty cache instead of sharing a stale one)
+    _meta: list = field(init=False, default_factory=list, repr=False, compare=False)
+    _dev: list = field(init=False, default_factory=list, repr=False, compare=False)   # staged device operands
 
     def __post_init__(self):
         n = len(self.alphas)
@@ -127,6 +130,11 @@ class PackedAdapters:
 
     # --- device metadata (segment index built by the C++ K8 builder) -------
     def meta(self) -> PackMeta:
+        if self._meta:
+            m = self._meta[0]
+            if (m.alphas != tuple(float(a) for a in self.alphas) or m.rank_offsets != tuple(self.rank_offsets)
+                    or m.row_offsets != tuple(self.row_offsets)):
+                self._meta.clear()
         if not self._meta:
             ranks = np.diff(self.rank_offsets)
             tokens = np.diff(self.row_offsets)
@@ -178,10 +186,67 @@ def _round_up(v: int, m: int) -> int:
     return (v + m - 1) // m * m
 
 
-class _Staged:
-    """bf16 device operands of one pack (padded for TMA: d, k -> multiples of 64)."""
+def _upload(a: np.ndarray, dev):
+    """numpy -> device in the caller's float dtype (converted to bf16 on the device: a host
+    fp64 -> fp32 pass over a 4096 x 14336 weight costs more than the PCIe copy itself),
+    through a page-locked block of torch's caching host allocator (async DMA; the host
+    copy of the next array overlaps it)."""
+    import torch
 
-    def __init__(self, packed: PackedAdapters, w_base: np.ndarray):
+    a = np.asarray(a)
+    if a.dtype not in (np.float64, np.float32):
+        a = a.astype(np.float64)
+    host = torch.empty(a.shape, dtype=torch.float64 if a.dtype == np.float64 else torch.float32, pin_memory=True)
+    np.copyto(host.numpy(), a)
+    return host.to(dev, non_blocking=True)
+
+
+def _fingerprint(a: np.ndarray) -> tuple:
+    """Identity of a host array for the staged-weight cache: buffer address, layout and
+    a strided sample of up to 4096 values (catches re-filled buffers)."""
+    flat = a.reshape(-1) if a.flags.c_contiguous else np.ascontiguousarray(a).reshape(-1)
+    step = max(1, flat.size // 4096)
+    return (a.__array_interface__["data"][0], a.shape, a.strides, a.dtype.str, flat[::step].tobytes())
+
+
+class _WeightCache:
+    """Staged bf16 base weights, reused while the caller passes the same (unchanged) array
+    -- the forward and backward of one pack, or a loop over packs on one frozen base.
+    At most two weights stay resident."""
+
+    def __init__(self, size: int = 2):
+        self.size = size
+        self.entries: list = []   # (weakref to the array, fingerprint, device, staged tensor)
+
+    def get(self, w: np.ndarray, dev, dp: int, kp: int):
+        import weakref
+
+        import torch
+
+        fp = _fingerprint(w)
+        for e in self.entries:
+            ref, efp, edev, t = e
+            if ref() is w and efp == fp and edev == dev:
+                return t
+        t = torch.zeros((dp, kp), dtype=torch.bfloat16, device=dev)   # reference layout [d][k]
+        t[: w.shape[0], : w.shape[1]] = _upload(w, dev).to(torch.bfloat16)
+        try:
+            ref = weakref.ref(w)
+        except TypeError:   # not weak-referenceable: never reused
+            return t
+        self.entries = [e for e in self.entries if e[0]() is not None][-(self.size - 1):] + [(ref, fp, dev, t)]
+        return t
+
+
+_W_CACHE = _WeightCache()
+
+
+class _Staged:
+    """bf16 device operands of one pack (padded for TMA: d, k -> multiples of 64).  Built
+    once per PackedAdapters instance (the frozen dataclass's fields never change) and
+    kept with it, so packed_backward reuses packed_forward's X, adapters and Hs."""
+
+    def __init__(self, packed: PackedAdapters):
         import torch
 
         if not torch.cuda.is_available():
@@ -196,36 +261,47 @@ class _Staged:
         self.d, self.k, self.T, self.n = d, k, T, n
         self.dp, self.kp = _round_up(d, 64), _round_up(k, 64)
         bf = torch.bfloat16
-
-        def to_dev(a):
-            # upload in the caller's dtype and convert on the device: a host-side fp64 -> fp32
-            # pass over a 4096 x 14336 weight costs more than the PCIe copy itself
-            a = np.asarray(a)
-            if a.dtype not in (np.float64, np.float32):
-                a = a.astype(np.float64)
-            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-
         self.x = torch.zeros((T, self.dp), dtype=bf, device=dev)
         if T:
-            self.x[:, :d] = to_dev(packed.inputs).to(bf)
-        self.w = torch.zeros((self.dp, self.kp), dtype=bf, device=dev)  # reference layout [d][k]
-        self.w[:d, :k] = to_dev(w_base).to(bf)
+            self.x[:, :d] = _upload(packed.inputs, dev).to(bf)
         R64 = m.rpad64
         self.a_sh = torch.zeros((n, self.dp, R64), dtype=bf, device=dev)
         self.bt_sh = torch.zeros((n, self.kp, R64), dtype=bf, device=dev)
+        down = _upload(packed.down_block, dev).to(bf)     # one transfer per block, split on the device
+        up_t = _upload(packed.up_block, dev).to(bf).t()
         for i in range(n):
             rs = packed.rank_slice(i)
             r = rs.stop - rs.start
-            self.a_sh[i, :d, :r] = to_dev(packed.down_block[:, rs]).to(bf)
-            self.bt_sh[i, :k, :r] = to_dev(packed.up_block[rs, :].T).to(bf)
+            self.a_sh[i, :d, :r] = down[:, rs]
+            self.bt_sh[i, :k, :r] = up_t[:, rs]
+        self.hs = None
 
-    def forward(self):
+    @classmethod
+    def of(cls, packed: PackedAdapters) -> "_Staged":
+        import torch
+
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+        st = packed._dev[0] if packed._dev else None
+        if st is None or st.dev.index != dev:
+            st = cls(packed)
+            packed._dev[:] = [st]
+        return st
+
+    def hidden(self):
+        """Hs = alpha_i X_i A_i (K2a), computed once per pack."""
         from . import ops
 
-        y, hs = ops.linear_fwd(self.meta, self.x, self.w, False, self.a_sh, self.bt_sh,
-                               y_out=self.torch.empty((self.T, self.kp), dtype=self.torch.bfloat16,
-                                                      device=self.dev))
-        return y, hs
+        if self.hs is None:
+            self.hs = self.torch.empty((self.T, self.meta.rpad64), dtype=self.torch.bfloat16, device=self.dev)
+            ops.shrink(self.meta, self.x, self.a_sh, self.hs)
+        return self.hs
+
+    def forward(self, w):
+        from . import ops
+
+        y = self.torch.empty((self.T, self.kp), dtype=self.torch.bfloat16, device=self.dev)
+        ops.linear_expand(self.meta, self.x, w, False, self.bt_sh, self.hidden(), y_out=y)
+        return y
 
 
 def _out_dtype(*arrays) -> np.dtype:
@@ -246,6 +322,10 @@ def _to_host(t, dtype: np.dtype) -> np.ndarray:
     return host.numpy().astype(dtype, copy=False)
 
 
+def _staged_weight(packed: PackedAdapters, w_base: np.ndarray, st: _Staged):
+    return _W_CACHE.get(np.asarray(w_base), st.dev, st.dp, st.kp)
+
+
 def packed_forward(packed: PackedAdapters, w_base: np.ndarray) -> list[np.ndarray]:
     """Per-adapter outputs y_i = x_i W + alpha_i (x_i A_i) B_i (reference lorapack.py:183-199).
 
@@ -253,8 +333,8 @@ def packed_forward(packed: PackedAdapters, w_base: np.ndarray) -> list[np.ndarra
     tcgen05 base GEMM whose tiles add Hs_i B_i as extra K-steps."""
     if w_base.shape != (packed.d, packed.k):
         raise ValueError(f"base weight must be ({packed.d}, {packed.k}), got {w_base.shape}")
-    st = _Staged(packed, w_base)
-    y, _ = st.forward()
+    st = _Staged.of(packed)
+    y = st.forward(_staged_weight(packed, w_base, st))
     host = _to_host(y[:, : packed.k], _out_dtype(packed.inputs, w_base))
     return [host[packed.row_slice(i)] for i in range(packed.adapter_count)]
 
@@ -263,9 +343,10 @@ def packed_backward(packed: PackedAdapters, w_base: np.ndarray, upstreams: Seque
                     ) -> tuple[list[np.ndarray], list[np.ndarray], list[np.ndarray]]:
     """Per-adapter (d_down, d_up, d_input) (reference lorapack.py:202-231).
 
-    Runs K2a (recomputing Hs as the reference does), then Case 2 (K4 shrink),
-    Case 1 (K3), Case 3 (K5) segment reductions and Case 4 (K6 GEMM with the
-    LoRA term as extra K-steps)."""
+    Hs = alpha X A comes from this pack's forward when it ran (else one K2a shrink: the
+    reference recomputes ``hidden = X @ A_all``, :216), then Case 2 (K4 shrink), Case 1
+    (K3), Case 3 (K5) segment reductions and Case 4 (K6 GEMM with the LoRA term as extra
+    K-steps)."""
     if len(upstreams) != packed.adapter_count:
         raise ValueError(f"{packed.adapter_count} adapters but {len(upstreams)} upstream gradients")
     for i, dy in enumerate(upstreams):
@@ -277,23 +358,22 @@ def packed_backward(packed: PackedAdapters, w_base: np.ndarray, upstreams: Seque
         raise ValueError(f"base weight must be ({packed.d}, {packed.k}), got {w_base.shape}")
     from . import ops
 
-    st = _Staged(packed, w_base)
+    st = _Staged.of(packed)
     torch = st.torch
     m = st.meta
-    _, hs = st.forward()
+    w = _staged_weight(packed, w_base, st)
+    hs = st.hidden()
     dy = torch.zeros((st.T, st.kp), dtype=torch.bfloat16, device=st.dev)
     if st.T:
         ups = np.concatenate([np.asarray(u) for u in upstreams], axis=0)
-        if ups.dtype not in (np.float64, np.float32):
-            ups = ups.astype(np.float64)
-        dy[:, : st.k] = torch.from_numpy(ups).to(st.dev).to(torch.bfloat16)
+        dy[:, : st.k] = _upload(ups, st.dev).to(torch.bfloat16)
     R16 = m.rpad16_total
     grad_a = torch.empty(st.dp * R16, dtype=torch.float32, device=st.dev)
     grad_b = torch.empty(st.kp * R16, dtype=torch.float32, device=st.dev)
-    dx = ops.linear_bwd(m, st.x, st.w, False, st.a_sh, st.bt_sh, hs, dy, grad_a, grad_b)
+    dx = ops.linear_bwd(m, st.x, w, False, st.a_sh, st.bt_sh, hs, dy, grad_a, grad_b)
     dt = _out_dtype(packed.inputs, w_base, *upstreams)
-    ga = grad_a.cpu().numpy()
-    gb = grad_b.cpu().numpy()
+    ga = _to_host(grad_a, np.float32)
+    gb = _to_host(grad_b, np.float32)
     dxh = _to_host(dx[:, : st.d], dt)
     d_downs, d_ups, d_inputs = [], [], []
     for i in range(packed.adapter_count):
@@ -361,17 +441,19 @@ def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: 
            for i in range(n)]
     d_downs, d_ups, d_inputs = packed_backward(packed, w_base, ups)
 
-    st = _Staged(packed, w_base)
+    st = _Staged(packed)          # a private copy: its operands are perturbed in place below
     torch = st.torch
     m = st.meta
+    w = _staged_weight(packed, w_base, st)
     dy = torch.zeros((st.T, st.kp), dtype=torch.float64, device=st.dev)
     if st.T:
         dy[:, : st.k] = torch.from_numpy(np.concatenate(ups, axis=0)).to(st.dev)
-    _, hs = st.forward()
+    hs = st.hidden()
+    hs_pert = torch.empty_like(hs)
     y = torch.empty((st.T, st.kp), dtype=torch.bfloat16, device=st.dev)
 
     def loss(hs_t) -> float:
-        ops.linear_expand(m, st.x, st.w, False, st.bt_sh, hs_t, y_out=y)
+        ops.linear_expand(m, st.x, w, False, st.bt_sh, hs_t, y_out=y)
         return float((y.double() * dy).sum().item())
 
     def fd(tensor, index, recompute_hs: bool) -> float:
@@ -380,9 +462,12 @@ def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: 
         for sgn in (1.0, -1.0):
             tensor[index] = (orig.double() + sgn * step).to(tensor.dtype)
             pos.append(float(tensor[index].double().item()))
-            h = st.forward()[1] if recompute_hs else hs
+            h = ops.shrink(m, st.x, st.a_sh, hs_pert) if recompute_hs else hs
             vals.append(loss(h))
         tensor[index] = orig
+        if pos[0] == pos[1]:
+            raise ValueError(f"grad_check step {step} vanishes in the bf16 operands (no representable "
+                             f"perturbation of {float(orig.double().item())}); use a larger step")
         return (vals[0] - vals[1]) / (pos[0] - pos[1])
 
     errs = {}
@@ -409,7 +494,7 @@ def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: 
     dyb = torch.zeros((st.T, st.kp), dtype=torch.bfloat16, device=st.dev)
     dyb.copy_(dy.to(torch.bfloat16))
     dh = torch.empty((st.T, m.rpad64), dtype=torch.bfloat16, device=st.dev)
-    ops.linear_bwd(m, st.x, st.w, False, st.a_sh, st.bt_sh, hs, dyb, None, None, need_dx=False,
+    ops.linear_bwd(m, st.x, w, False, st.a_sh, st.bt_sh, hs, dyb, None, None, need_dx=False,
                    dh_ws=dh)
     an_h = dh.float().cpu().numpy()
     worst = 0.0
@@ -429,6 +514,8 @@ def grad_check(packed: PackedAdapters, w_base: np.ndarray, seed: int = 0, step: 
                         pos.append(float(hs[t, j].double().item()) / alpha)
                         vals.append(loss(hs))
                     hs[t, j] = orig
+                    if pos[0] == pos[1]:
+                        raise ValueError(f"grad_check step {step} vanishes in the bf16 hidden activations")
                     num = (vals[0] - vals[1]) / (pos[0] - pos[1])
                 worst = max(worst, _rel_err(np.array([an_h[t, j]]), np.array([num])))
     errs["up_input"] = worst

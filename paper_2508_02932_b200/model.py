@@ -702,10 +702,12 @@ class PackedLoraTrainer:
         return losses
 
     # ------------------------------------------------------------------ data
-    def synthetic_tokens(self, seed_base: int = 1000) -> torch.Tensor:
-        """tokens ~ U{0..V-1}, seed 1000+i per adapter."""
+    def synthetic_tokens(self, seed_base: int = 1000, seeds: Sequence[int] | None = None) -> torch.Tensor:
+        """tokens ~ U{0..V-1}, seed 1000+i per adapter; ``seeds``
+        overrides the per-adapter seeds (a rank of a planner split keeps the seeds of its
+        adapters' positions in the whole workload)."""
         parts = []
         for i, sp in enumerate(self.specs):
-            g = torch.Generator(device="cpu").manual_seed(seed_base + i)
+            g = torch.Generator(device="cpu").manual_seed(seed_base + i if seeds is None else int(seeds[i]))
             parts.append(torch.randint(0, self.cfg.vocab, (sp.batch * self.s,), generator=g))
         return torch.cat(parts)

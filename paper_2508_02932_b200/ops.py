@@ -90,6 +90,26 @@ def _need(t: torch.Tensor | None, name: str, dtype=torch.bfloat16, allow_none=Fa
     return t.data_ptr()
 
 
+def _on_current_device(t: torch.Tensor, name: str) -> None:
+    """libplora launches on the current device's stream: operands of another device would
+    be dereferenced on the wrong GPU."""
+    if t.is_cuda and t.device.index != torch.cuda.current_device():
+        raise ValueError(f"{name} is on {t.device} but the current device is cuda:{torch.cuda.current_device()} "
+                         f"(run the op under torch.cuda.device({t.device.index}))")
+
+
+def _size(t: torch.Tensor | None, name: str, numel: int) -> None:
+    """Kernels write through raw pointers: a buffer smaller than the pack needs would be an
+    out-of-bounds device write, so sizes are checked against the pack metadata here."""
+    if t is not None and t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, the pack needs {numel}")
+
+
+def _lora_shapes(meta: PackMeta, K: int, l_sh: torch.Tensor, out: torch.Tensor, T: int) -> None:
+    _size(l_sh, "lora operand", meta.n_adapters * K * meta.rpad64)
+    _size(out, "low-rank output", T * meta.rpad64)
+
+
 def gemm(a: torch.Tensor, w: torch.Tensor, w_kmajor: bool = True, out: torch.Tensor | None = None,
          residual: torch.Tensor | None = None) -> torch.Tensor:
     """out[M][N] = a[M][K] @ (w.T if w_kmajor else w) (+ residual), bf16, tcgen05."""
@@ -97,8 +117,10 @@ def gemm(a: torch.Tensor, w: torch.Tensor, w_kmajor: bool = True, out: torch.Ten
     N = w.shape[0] if w_kmajor else w.shape[1]
     if (w.shape[1] if w_kmajor else w.shape[0]) != K:
         raise ValueError(f"gemm: weight {tuple(w.shape)} does not match K={K}")
+    _on_current_device(a, "a")
     if out is None:
         out = torch.empty((M, N), dtype=torch.bfloat16, device=a.device)
+    _size(out, "out", M * N)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_gemm_bf16(
         _stream(), M, N, K, _need(a, "a"), _need(w, "w"), int(w_kmajor), _need(out, "out"),
@@ -121,6 +143,9 @@ def linear_fwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
         hs_out = torch.empty((T, meta.rpad64), dtype=torch.bfloat16, device=x.device)
     if y_out is None:
         y_out = torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
+    _on_current_device(x, "x")
+    _lora_shapes(meta, d, a_sh, hs_out, T)
+    _size(bt_sh, "bt_sh", meta.n_adapters * k * meta.rpad64)
     s = meta.struct
     if _TIMER is not None:
         shrink(meta, x, a_sh, hs_out)
@@ -137,6 +162,8 @@ def linear_fwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
 def shrink(meta: PackMeta, p: torch.Tensor, l_sh: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     """K2a / K4: out = alpha_i * p_i @ L_i  (L_sh [n][K][rpad64])."""
     T, K = p.shape
+    _on_current_device(p, "p")
+    _lora_shapes(meta, K, l_sh, out, meta.total_tokens)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_lora_shrink(_stream(), ctypes.byref(meta.struct), K, _need(p, "p"),
                                             _need(l_sh, "l_sh"), _need(out, "out")), "plora_lora_shrink")
@@ -150,6 +177,9 @@ def shrink(meta: PackMeta, p: torch.Tensor, l_sh: torch.Tensor, out: torch.Tenso
 def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
     """K3 / K5: G_i = p_i^T q_i per token segment, fp32 into the adapter-major region g."""
     T, Mdim = p.shape
+    _on_current_device(p, "p")
+    _size(q, "q", meta.total_tokens * meta.rpad64)
+    _size(g, "g", Mdim * meta.rpad16_total)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_lora_segred(_stream(), ctypes.byref(meta.struct), Mdim, _need(p, "p"),
                                             _need(q, "q"), _need(g, "g", torch.float32)), "plora_lora_segred")
@@ -169,6 +199,9 @@ def shrink_multi(meta: PackMeta, p: torch.Tensor, l_shs, outs) -> list:
     """K2a for targets sharing the input p (q/k/v or gate/up): outs[j] = alpha_i p_i L_j,i,
     p read once (one launch when every rank <= 64)."""
     T, K = p.shape
+    _on_current_device(p, "p")
+    for j, (l_sh, out) in enumerate(zip(l_shs, outs)):
+        _lora_shapes(meta, K, l_sh, out, meta.total_tokens)
     t = _TIMER.start() if _TIMER else None
     lp, _k1 = _ptr_array(l_shs, "l_sh")
     op, _k2 = _ptr_array(outs, "out")
@@ -185,6 +218,10 @@ def shrink_multi(meta: PackMeta, p: torch.Tensor, l_shs, outs) -> list:
 def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
     """K5 for targets sharing p: G_j,i = p_i^T Q_j,i (fp32, adapter-major regions), p read once."""
     T, Mdim = p.shape
+    _on_current_device(p, "p")
+    for q, g in zip(qs, gs):
+        _size(q, "q", meta.total_tokens * meta.rpad64)
+        _size(g, "g", Mdim * meta.rpad16_total)
     t = _TIMER.start() if _TIMER else None
     qp, _k1 = _ptr_array(qs, "q")
     gp, _k2 = _ptr_array(gs, "g", torch.float32)
@@ -203,7 +240,11 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
     """K1 + K2b for targets sharing x (q/k/v, gate/up) in ONE pair-GEMM launch:
     y_j = x op(W_j) + Hs_j,i B_j,i (+ bias_j, in the epilogue) (returns the new y_j [T][k_j])."""
     T, d = x.shape
+    _on_current_device(x, "x")
     ks = [w.shape[0] if w_kmajor else w.shape[1] for w in ws]
+    for k, bt, hs in zip(ks, bt_shs, hss):
+        _size(bt, "bt_sh", meta.n_adapters * k * meta.rpad64)
+        _size(hs, "hs", T * meta.rpad64)
     ys = list(y_outs) if y_outs is not None else [torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
                                                    for k in ks]
     karr = (ctypes.c_int64 * len(ks))(*ks)
@@ -236,6 +277,11 @@ def linear_gate_up_swiglu(meta: PackMeta, x: torch.Tensor, w_gate: torch.Tensor,
     (g, u, act), act = silu(g) u bit-identical to elementwise.swiglu_fwd(g, u)."""
     T, d = x.shape
     ffn = w_gate.shape[0]
+    _on_current_device(x, "x")
+    for nm, t_ in (("bt_gate", bt_gate), ("bt_up", bt_up)):
+        _size(t_, nm, meta.n_adapters * ffn * meta.rpad64)
+    for nm, t_ in (("hs_gate", hs_gate), ("hs_up", hs_up)):
+        _size(t_, nm, T * meta.rpad64)
     if outs is not None:
         g, u, act = outs
     else:
@@ -260,6 +306,10 @@ def linear_dx_group(meta: PackMeta, dys, ws, a_shs, dhs, d: int, w_kmajor: bool 
     (one fp32 accumulator over the concatenated K range)."""
     T = dys[0].shape[0]
     ks = [dy.shape[1] for dy in dys]
+    _on_current_device(dys[0], "dy")
+    for a_sh, dh in zip(a_shs, dhs):
+        _size(a_sh, "a_sh", meta.n_adapters * d * meta.rpad64)
+        _size(dh, "dh", T * meta.rpad64)
     if dx_out is None:
         dx_out = torch.empty((T, d), dtype=torch.bfloat16, device=dys[0].device)
     karr = (ctypes.c_int64 * len(ks))(*ks)
@@ -288,6 +338,9 @@ def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bo
     k = w.shape[0] if w_kmajor else w.shape[1]
     if y_out is None:
         y_out = torch.empty((T, k), dtype=torch.bfloat16, device=x.device)
+    _on_current_device(x, "x")
+    _size(bt_sh, "bt_sh", meta.n_adapters * k * meta.rpad64)
+    _size(hs, "hs", T * meta.rpad64)
     s = meta.struct
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_linear_expand(
@@ -314,6 +367,14 @@ def linear_bwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
         dh_ws = torch.empty((T, meta.rpad64), dtype=torch.bfloat16, device=x.device)
     if need_dx and dx_out is None:
         dx_out = torch.empty((T, d), dtype=torch.bfloat16, device=x.device)
+    _on_current_device(x, "x")
+    _size(a_sh, "a_sh", meta.n_adapters * d * meta.rpad64)
+    _size(bt_sh, "bt_sh", meta.n_adapters * k * meta.rpad64)
+    _size(hs, "hs", T * meta.rpad64)
+    _size(dh_ws, "dh_ws", T * meta.rpad64)
+    _size(dy, "dy", T * k)
+    _size(grad_a, "grad_a", d * meta.rpad16_total)
+    _size(grad_b, "grad_b", k * meta.rpad16_total)
     s = meta.struct
     if _TIMER is not None:
         shrink(meta, dy, bt_sh, dh_ws)                       # Case 2 (K4)
@@ -351,3 +412,92 @@ def adamw(chunks: torch.Tensor, param: torch.Tensor, grad: torch.Tensor, exp_avg
     if t is not None:
         # 30 B per trainable parameter: read p,g,m,v (16) + write p,m,v (12) + bf16 shadow (2)
         _TIMER.stop("adamw", t, nbytes=30.0 * (algo_params if algo_params is not None else param.numel()))
+
+
+# ------------------------------------------------------------------ torch training op
+class PackedLoraLinearFn(torch.autograd.Function):
+    """Autograd op over plora_linear_fwd / plora_linear_bwd: the training form of the
+    reference ``packed_forward`` / ``packed_backward`` (lorapack.py:183-231).
+
+    Differentiable inputs: ``x`` [T][d] bf16 (tokens adapter-major, segments of ``meta``)
+    and the fp32 LoRA masters in the region layout the kernels write gradients into
+    (adapters.py): ``a_master`` = A_i [d][rpad16_i] blocks, ``b_master`` = B_i^T
+    [k][rpad16_i] blocks, back to back.  The forward reads their bf16 shadows
+    ``a_sh`` [n][d][64nb] / ``bt_sh`` [n][k][64nb] (kept equal to the masters by the
+    caller, see PackedLoraLinear).  Saved for the backward: x and Hs = alpha_i X_i A_i
+    (the reference recomputes ``hidden``, :216; here it is kept from the forward)."""
+
+    @staticmethod
+    def forward(ctx, x, a_master, b_master, meta, w, a_sh, bt_sh, w_kmajor=True):
+        y, hs = linear_fwd(meta, x, w, w_kmajor, a_sh, bt_sh)
+        ctx.save_for_backward(x, hs)
+        ctx.meta, ctx.w, ctx.a_sh, ctx.bt_sh, ctx.w_kmajor = meta, w, a_sh, bt_sh, w_kmajor
+        ctx.shapes = (a_master.shape, b_master.shape)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, hs = ctx.saved_tensors
+        need_x, need_a, need_b = ctx.needs_input_grad[:3]
+        dev = x.device
+        ga = torch.empty(ctx.shapes[0], dtype=torch.float32, device=dev) if need_a else None
+        gb = torch.empty(ctx.shapes[1], dtype=torch.float32, device=dev) if need_b else None
+        dx = linear_bwd(ctx.meta, x, ctx.w, ctx.w_kmajor, ctx.a_sh, ctx.bt_sh, hs, dy.contiguous(), ga, gb,
+                        need_dx=need_x)
+        return dx, ga, gb, None, None, None, None, None
+
+
+class PackedLoraLinear(torch.nn.Module):
+    """A frozen bf16 base projection with n packed LoRA adapters (heterogeneous rank and
+    alpha) over token segments: y_t = x_t W^T + alpha_i (x_t A_i) B_i for token t of
+    adapter i.  Parameters ``a`` / ``b`` are the fp32 masters (region layout); any torch
+    optimizer may update them -- the bf16 shadows are refreshed before the next forward
+    when a parameter's version changed.  ``weight`` is nn.Linear-layout [k][d] bf16."""
+
+    def __init__(self, meta: PackMeta, weight: torch.Tensor, init_std: float = 0.02, seed: int = 0):
+        super().__init__()
+        dev = weight.device
+        self.meta = meta.to(dev)
+        k, d = weight.shape
+        self.d, self.k = d, k
+        self.register_buffer("weight", weight.detach().to(torch.bfloat16).contiguous(), persistent=False)
+        R16, R64, n = meta.rpad16_total, meta.rpad64, meta.n_adapters
+        g = torch.Generator(device=dev).manual_seed(seed)
+        a = torch.zeros(d * R16, dtype=torch.float32, device=dev)
+        b = torch.zeros(k * R16, dtype=torch.float32, device=dev)
+        self.a = torch.nn.Parameter(a)
+        self.b = torch.nn.Parameter(b)
+        for i in range(n):
+            r = meta.ranks[i]
+            self.block("a", i)[:, :r] = (torch.rand(d, r, generator=g, device=dev) * 2 - 1) / d ** 0.5
+            self.block("b", i)[:, :r] = torch.randn(k, r, generator=g, device=dev) * init_std
+        self.register_buffer("a_sh", torch.zeros((n, d, R64), dtype=torch.bfloat16, device=dev), persistent=False)
+        self.register_buffer("bt_sh", torch.zeros((n, k, R64), dtype=torch.bfloat16, device=dev), persistent=False)
+        self._versions = None
+
+    def block(self, which: str, i: int) -> torch.Tensor:
+        """Adapter i's fp32 block: A_i [d][rpad16_i] ("a") or B_i^T [k][rpad16_i] ("b")."""
+        p, rows = (self.a, self.d) if which == "a" else (self.b, self.k)
+        ro = self.meta.rpad_off
+        return p.data[rows * int(ro[i]): rows * int(ro[i + 1])].view(rows, int(ro[i + 1] - ro[i]))
+
+    def down(self, i: int) -> torch.Tensor:
+        """Reference-layout A_i (d x r)."""
+        return self.block("a", i)[:, : self.meta.ranks[i]]
+
+    def up(self, i: int) -> torch.Tensor:
+        """Reference-layout B_i (r x k)."""
+        return self.block("b", i)[:, : self.meta.ranks[i]].t()
+
+    @torch.no_grad()
+    def refresh_shadows(self) -> None:
+        for i in range(self.meta.n_adapters):
+            rp = int(self.meta.rpad_off[i + 1] - self.meta.rpad_off[i])
+            self.a_sh[i, :, :rp] = self.block("a", i).to(torch.bfloat16)
+            self.bt_sh[i, :, :rp] = self.block("b", i).to(torch.bfloat16)
+        self._versions = (self.a._version, self.b._version)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if self._versions != (self.a._version, self.b._version):
+            self.refresh_shadows()
+        return PackedLoraLinearFn.apply(x, self.a, self.b, self.meta, self.weight, self.a_sh, self.bt_sh, True)

@@ -29,19 +29,30 @@ from dataclasses import asdict, dataclass
 from typing import Callable, Sequence
 
 from .planner import JobQueue, Placement, place
-from .workload import LoraConfig, ProfileRecord
+from .trace import ScheduleTrace, TraceJob, check_feasibility
+from .workload import GpuPool, LoraConfig, ProfileRecord
 
 
 @dataclass(frozen=True)
 class JobRecord:
+    """One job as one device ran it.  ``start_s``/``end_s``: seconds since the shared
+    start barrier of all ranks (wall clock); ``device_start_s``: the device's own busy
+    clock at the job's start (when one process emulates several devices back to back,
+    this is the job's start on the emulated device); ``train_s``: the timed steps only."""
     job_id: str
     device: int
     configs: tuple
     steps: int
     start_s: float
-    duration_s: float
+    end_s: float
+    device_start_s: float
+    train_s: float
     iter_time_s: float
     losses: tuple = ()
+
+    @property
+    def duration_s(self) -> float:
+        return self.end_s - self.start_s
 
 
 def rank_schedule(queue: JobQueue, placement: Placement, rank: int) -> list:
@@ -125,37 +136,69 @@ def tp_groups(queue: JobQueue, placement: Placement, world: int, gpu_count: int,
     return out
 
 
+def _device_guard(dev: int):
+    """Run a job with its device current: libplora launches on the current device's
+    stream, so tensors of cuda:dev must be used with dev current."""
+    import contextlib
+
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.device(dev % max(1, torch.cuda.device_count()))
+    except Exception:  # pragma: no cover
+        pass
+    return contextlib.nullcontext()
+
+
 def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, rank: int = 0, world: int = 1,
             model_name: str = "llama-3.1-8b", run_job: Callable | None = None,
             steps_override: int | None = None, all_gather: Callable | None = None,
-            new_group: Callable | None = None, checkpoint_dir=None) -> dict:
-    """Execute this rank's share of the queue.  Returns a report with the per-job records
-    (gathered from every rank when ``all_gather`` is given), profile records, the
-    measured makespan (max over ranks of the per-device busy time) and the placement."""
+            new_group: Callable | None = None, checkpoint_dir=None, pool: GpuPool | None = None) -> dict:
+    """Execute this rank's share of the queue and return the report of the whole queue.
+
+    One process per GPU (world == gpu_count): rank r runs the jobs placed on device r in
+    planned start order, with device r current; all ranks start from one barrier
+    (``all_gather``) and every job records its wall-clock start / end since that
+    barrier, so ``makespan_s`` is the measured wall-clock makespan of the queue.  A
+    degree-d job starts on all d ranks together (its process group synchronises them).
+    With fewer processes than GPUs (one box with one GPU emulating a larger pool), a rank
+    drives every device = rank (mod world) back to back; the trace then uses each
+    device's busy clock (``clock == "device"``, a lower bound of the real makespan).
+    The executed trace is checked against the queue with ``check_feasibility``
+    (reference simulator.py:154-211); violations are reported, not raised."""
     placement = place(queue, gpu_count)
     groups = tp_groups(queue, placement, world, gpu_count, new_group)
     by_id = {c.id: c for c in configs}
-    devices = list(range(rank, gpu_count, world))   # a rank drives every device = rank (mod world)
+    devices = list(range(rank, gpu_count, world))
+    emulated = world < gpu_count
+    if all_gather is not None:
+        all_gather(None)                      # shared start barrier
+    t0 = time.perf_counter()
     records = []
-    t_dev = {}
     for dev in devices:
         clock = 0.0
         for job in rank_schedule(queue, placement, dev):
             comm = groups.get(placement.devices[job.id])
             extra = {"tp": comm} if comm is not None else {}
-            if run_job is None:
-                steps, dt, it, losses = train_packed_job(job, by_id, model_name, f"cuda:{dev % max(1, _ndev())}",
-                                                         steps_override, checkpoint_dir=checkpoint_dir, **extra)
-            else:
-                steps, dt, it, losses = run_job(job, by_id, dev, **extra)
-            records.append(JobRecord(job.id, dev, job.configs, steps, clock, dt, it, tuple(losses)))
-            clock += dt
-        t_dev[dev] = clock
-    local = {"records": [asdict(r) for r in records], "busy_s": t_dev}
+            s = time.perf_counter() - t0
+            with _device_guard(dev):
+                if run_job is None:
+                    steps, dt, it, losses = train_packed_job(job, by_id, model_name, _cuda(dev), steps_override,
+                                                             checkpoint_dir=checkpoint_dir, **extra)
+                else:
+                    steps, dt, it, losses = run_job(job, by_id, dev, **extra)
+            e = time.perf_counter() - t0
+            records.append(JobRecord(job.id, dev, job.configs, steps, s, e, clock, dt, it, tuple(losses)))
+            clock += e - s
+    local = {"records": [asdict(r) for r in records]}
     gathered = all_gather(local) if all_gather is not None else [local]
     all_records = [JobRecord(**{**r, "configs": tuple(r["configs"]), "losses": tuple(r["losses"])})
                    for g in gathered for r in g["records"]]
-    busy = {int(k): v for g in gathered for k, v in g["busy_s"].items()}
+    busy: dict = {}
+    for r in all_records:
+        busy[r.device] = busy.get(r.device, 0.0) + r.duration_s
+    trace = executed_trace(queue, all_records, gpu_count, clock="device" if emulated else "wall")
+    violations = check_feasibility(trace, queue, pool)
     # one profile record per job (a TP job reports from each of its ranks: keep the slowest)
     degree = {j.id: j.degree for j in queue.jobs()}
     per_job: dict = {}
@@ -166,8 +209,36 @@ def execute(queue: JobQueue, configs: Sequence[LoraConfig], gpu_count: int, *, r
                               tuple(by_id[c].batch_size for c in r.configs),
                               max(by_id[c].seq_len for c in r.configs), r.iter_time_s)
                 for _, r in sorted(per_job.items())]
-    return {"records": all_records, "profiles": profiles, "makespan_s": max(busy.values(), default=0.0),
-            "busy_s": busy, "placement": placement}
+    return {"records": all_records, "profiles": profiles, "makespan_s": trace.makespan, "clock": trace.clock,
+            "busy_s": busy, "placement": placement, "trace": trace, "violations": violations}
+
+
+def executed_trace(queue: JobQueue, records: Sequence[JobRecord], gpu_count: int, clock: str = "wall"
+                   ) -> ScheduleTrace:
+    """The schedule that ran: one TraceJob per executed job id, on every device that ran
+    it, from the earliest start to the latest end over those devices (wall clock), or on
+    the device busy clocks (``clock == "device"``)."""
+    predicted = {j.id: j for j in queue.jobs()}
+    by_job: dict = {}
+    for r in records:
+        by_job.setdefault(r.job_id, []).append(r)
+    jobs = []
+    for jid, rs in sorted(by_job.items(), key=lambda kv: (min(r.start_s for r in kv[1]), kv[0])):
+        if clock == "wall":
+            s, e = min(r.start_s for r in rs), max(r.end_s for r in rs)
+        else:
+            s = min(r.device_start_s for r in rs)
+            e = max(r.device_start_s + r.duration_s for r in rs)
+        p = predicted.get(jid)
+        jobs.append(TraceJob(job_id=jid, configs=tuple(rs[0].configs), degree=p.degree if p else len(rs),
+                             start_s=s, duration_s=e - s, devices=tuple(sorted({r.device for r in rs})),
+                             predicted_s=p.predicted_time if p else 0.0))
+    return ScheduleTrace(jobs=tuple(jobs), makespan=max((j.end_s for j in jobs), default=0.0),
+                         gpu_count=gpu_count, clock=clock)
+
+
+def _cuda(dev: int) -> str:
+    return f"cuda:{dev % max(1, _ndev())}"
 
 
 def _ndev() -> int:
@@ -179,5 +250,5 @@ def _ndev() -> int:
 
 
 def report_json(rep: dict) -> str:
-    return json.dumps({"makespan_s": rep["makespan_s"], "busy_s": rep["busy_s"],
-                       "jobs": [asdict(r) for r in rep["records"]]}, indent=1)
+    return json.dumps({"makespan_s": rep["makespan_s"], "clock": rep["clock"], "busy_s": rep["busy_s"],
+                       "violations": rep["violations"], "jobs": [asdict(r) for r in rep["records"]]}, indent=1)

@@ -25,8 +25,10 @@ def _instance(n=10, G=4):
 
 
 def fake_run(job, by_id, dev):
+    import time
     steps = max(by_id[c].train_steps for c in job.configs)
     it = 0.1 + 0.01 * len(job.configs)
+    time.sleep(0.002 * len(job.configs))      # wall time the engine records
     return steps, steps * it, it, [1.0] * len(job.configs)
 
 
@@ -41,7 +43,8 @@ def _worker(rank, world, port, out):
 
     configs, queue, _ = _instance()
     rep = execute(queue, configs, 4, rank=rank, world=world, run_job=fake_run, all_gather=gather)
-    out[rank] = (rep["makespan_s"], sorted((r.job_id, r.device) for r in rep["records"]), rep["busy_s"])
+    out[rank] = (rep["makespan_s"], sorted((r.job_id, r.device) for r in rep["records"]), rep["busy_s"],
+                 rep["violations"], rep["clock"])
     dist.destroy_process_group()
 
 
@@ -64,7 +67,67 @@ def test_engine_two_ranks_gloo():
     assert r0[1] == expect                                 # each job ran once, on its placed device
     busy = r0[2]
     assert set(busy) == {0, 1, 2, 3}
+    # two processes drive four devices: device busy clocks, a valid execution of the queue
+    assert r0[4] == "device" and r0[3] == []
     assert r0[0] == pytest.approx(max(busy.values()))
+
+
+def _wall_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def gather(obj):
+        res = [None] * world
+        dist.all_gather_object(res, obj)
+        return res
+
+    configs, queue, _ = _instance(n=8, G=2)
+    rep = execute(queue, configs, 2, rank=rank, world=world, run_job=fake_run, all_gather=gather)
+    tr = rep["trace"]
+    out[rank] = (rep["clock"], rep["violations"], rep["makespan_s"], [(j.job_id, j.devices, j.start_s, j.end_s)
+                                                                      for j in tr.jobs])
+    dist.destroy_process_group()
+
+
+def test_engine_wall_clock_one_process_per_gpu():
+    """world == gpu_count: the makespan is the shared wall clock, the executed trace
+    passes the feasibility re-check, and jobs on one device never overlap."""
+    configs, queue, _ = _instance(n=8, G=2)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_wall_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    clock, violations, makespan, jobs = out[0]
+    assert clock == "wall" and violations == []
+    assert makespan == pytest.approx(max(e for _, _, _, e in jobs))
+    assert sorted(j for j, *_ in jobs) == sorted(j.id for j in queue.jobs())
+
+
+def test_check_feasibility_catches_bad_traces():
+    from paper_2508_02932_b200.sweep.trace import ScheduleTrace, TraceJob, check_feasibility
+
+    configs, queue, _ = _instance(n=6, G=2)
+    jobs = queue.jobs()
+    good = []
+    t = {0: 0.0, 1: 0.0}
+    for k, j in enumerate(jobs):
+        devs = (0, 1) if j.degree == 2 else (k % 2,)
+        s = max(t[d] for d in devs)
+        good.append(TraceJob(j.id, j.configs, j.degree, s, 1.0, devs, j.predicted_time))
+        for d in devs:
+            t[d] = s + 1.0
+    ok = ScheduleTrace(tuple(good), max(x.end_s for x in good), 2)
+    assert check_feasibility(ok, queue) == []
+    # two jobs on one device at the same time
+    bad = list(good)
+    bad[1] = TraceJob(jobs[1].id, jobs[1].configs, good[1].degree, good[0].start_s, 1.0, good[0].devices, 0.0)
+    v = check_feasibility(ScheduleTrace(tuple(bad), max(x.end_s for x in bad), 2), queue)
+    assert any("overlap on device(s)" in m for m in v)
+    # a job missing, a device outside the pool, a wrong makespan
+    v = check_feasibility(ScheduleTrace(tuple(good[1:]), 99.0, 2), queue)
+    assert any("executed 0 times" in m for m in v) and any("makespan" in m for m in v)
+    bad = list(good)
+    bad[0] = TraceJob(jobs[0].id, jobs[0].configs, 1, 0.0, 1.0, (5,), 0.0)   # also the wrong device count
+    assert any("outside the pool" in m for m in check_feasibility(ScheduleTrace(tuple(bad), ok.makespan, 2), queue))
 
 
 def test_rank_schedule_matches_placement_and_covers_queue():

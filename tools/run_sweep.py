@@ -1,25 +1,37 @@
-"""C5: Llama-3.1-8B hyper-parameter sweep (64 configs) -- plan, place, execute, report.
+"""C5: Llama-3.1-8B hyper-parameter sweep (64 configs) -- profile, calibrate, plan, place,
+execute on the GPUs of one box, validate the executed trace, report the measured
+wall-clock makespan beside the planner's prediction (reference cli.py:103-159).
 
-  python tools/run_sweep.py [--gpus 8] [--steps-measured 3] [--out gpurun_out/sweep.json]
+  python tools/run_sweep.py [--gpus 8] [--plans balanced,reference,min] [--out gpurun_out/sweep.json]
 
-1. profile: a few packed jobs of different sizes run on cuda:0 -> ProfileRecords (degree 1);
-2. calibrate: TimeModel per the reference least-squares fit, with the B200 token term
-   (grid-searched token_weight; load = r*b*s + w*b*s) -- degrees > 1 are costed d x the
-   degree-1 job because tensor-parallel jobs are not built yet (so the planner uses degree 1);
-3. plan: plan_jobs on 8 x B200 (memory model from the Llama-3.1-8B shapes), Min-GPU /
-   Max-GPU baselines, predicted makespans (placement timeline == reference simulator rule);
-4. execute: the engine runs every job of the planned queue for --steps-measured steps on
-   its placed (virtual) device; with one physical GPU the 8 devices' jobs run back to
-   back and each device's busy time is measured separately (jobs share no data, so the
-   8-GPU makespan is the max over devices); step times are scaled to train_steps.
+With --gpus N and N visible GPUs the tool starts N ranks (torch.distributed.run, one
+process per GPU; NCCL) and every rank executes the jobs placed on its device; the
+makespan is the shared wall clock from the start barrier to the last job's end, and
+the executed trace is re-checked with ``check_feasibility`` (reference
+simulator.py:154-211).  With fewer GPUs than --gpus (a one-GPU box) one process
+emulates the pool: each emulated device's jobs run back to back and the makespan is
+the largest device busy time (``clock: device``, a lower bound).
+
+1. profile: rank 0 trains 6 packs of 1 .. 16 configs for a few steps -> ProfileRecords;
+2. calibrate: TimeModel per the reference least-squares fit with the B200 token term
+   (grid-searched token_weight; load = r*b*s + w*b*s); degrees > 1 are costed d x the
+   degree-1 job (tensor parallelism pays off only when a job does not fit one GPU);
+3. plan: plan_jobs on the pool (memory model from the Llama-3.1-8B shapes) -- the B200
+   balanced queue, the reference DTM queue, the Min-GPU baseline -- and their predicted
+   makespans (``place`` reproduces the reference simulator's timeline);
+4. execute: the engine runs every job for its full train_steps on its placed device.
 """
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import time
+from pathlib import Path
 
-sys.path.insert(0, ".")
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 import numpy as np  # noqa: E402
@@ -27,6 +39,7 @@ import numpy as np  # noqa: E402
 from paper_2508_02932_b200 import sweep as S  # noqa: E402
 from paper_2508_02932_b200.model import PRESETS  # noqa: E402
 from paper_2508_02932_b200.sweep.engine import execute, train_packed_job  # noqa: E402
+from paper_2508_02932_b200.sweep.jobsplit import ACT_BYTES_PER_TOKEN  # noqa: E402
 
 
 def grid(train_steps=50, seq=1024):
@@ -34,25 +47,7 @@ def grid(train_steps=50, seq=1024):
     return S.enumerate_grid([5e-5, 1e-4, 2e-4, 4e-4], [1, 2], [8, 16, 32, 64], [16.0, 64.0], tmpl)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=8)
-    ap.add_argument("--steps-measured", type=int, default=3)
-    ap.add_argument("--mem-gb", type=float, default=178.0)
-    ap.add_argument("--out", default="gpurun_out/sweep.json")
-    args = ap.parse_args()
-    t_start = time.perf_counter()
-    cfg = PRESETS["llama-3.1-8b"]
-    configs = grid()
-    by_id = {c.id: c for c in configs}
-    # memory model: bf16 base; activations ~2.95 MB/token saved by the trainer (measured peak at T=32768)
-    # adapter state at the trainer's storage precision (fp32 master + bf16 shadow, fp32 grad / moments);
-    # on this grid the plans are identical to the reference's c_prec costing (activations dominate)
-    model = S.model_spec_from_config(cfg, c_prec=2, act_coeffs=(0.0, 2.95e6 / 2 / 2, 2.95e6 / 2 / 2),
-                                     state_bytes=S.STATE_BYTES_PLORA)
-    pool = S.GpuPool(args.gpus, int(args.mem_gb * 1e9), load_factor=0.9)
-
-    # 1. profile packs of 1 .. 16 configs at degree 1
+def calibrate(configs, by_id, model, pool, steps):
     rng = np.random.default_rng(0)
     packs = [[0], [5, 17], list(range(0, 64, 16)), list(range(3, 64, 8)), list(rng.choice(64, 12, replace=False)),
              list(range(1, 64, 4))]
@@ -60,7 +55,9 @@ def main():
     for p in packs:
         job = S.make_job([configs[i].id for i in p], 1, S.TimeModel(coeffs={1: (1.0, 0.0)}),
                          S.MemoryContext(model, pool, configs))
-        steps, dt, it, _ = train_packed_job(job, by_id, "llama-3.1-8b", "cuda:0", steps_override=args.steps_measured)
+        import torch
+        dev = f"cuda:{torch.cuda.current_device()}"   # the engine's device key: the base weights are shared
+        _, _, it, _ = train_packed_job(job, by_id, "llama-3.1-8b", dev, steps_override=steps)
         cf = [by_id[c] for c in job.configs]
         profiles.append(S.ProfileRecord(1, tuple(c.rank for c in cf), tuple(c.batch_size for c in cf), 1024, it))
         print(f"profile: {len(p)} configs, {sum(c.batch_size for c in cf)} seqs -> {it:.3f} s/iter", flush=True)
@@ -73,58 +70,98 @@ def main():
         if best is None or tm1.fit_rel_rmse[1] < best.fit_rel_rmse[1]:
             best = tm1
     b1, m1 = best.params(1)
-    # degree d > 1 would need tensor parallelism (not built): cost it as d x the degree-1 job so the
-    # planner never prefers it (using d GPUs for the time of one)
+    return {"base_s": b1, "marginal_s": m1, "token_weight": best.token_weight, "rel_rmse": best.fit_rel_rmse[1],
+            "profiles": [dict(ranks=list(p.packed_ranks), batch_sizes=list(p.packed_batch_sizes),
+                              iter_time_s=p.iter_time_s) for p in profiles]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=8)
+    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None, help="override every job's train_steps (default: full)")
+    ap.add_argument("--plans", default="balanced,reference,min")
+    ap.add_argument("--mem-gb", type=float, default=178.0)
+    ap.add_argument("--out", default="gpurun_out/sweep.json")
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    ndev = torch.cuda.device_count()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and ndev >= args.gpus:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        raise SystemExit(subprocess.call([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                          f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                          f"--master-port={port}", __file__, *sys.argv[1:]]))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local % max(1, ndev))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local % max(1, ndev)))
+
+    def gather(obj):
+        if world == 1:
+            return [obj]
+        res = [None] * world
+        dist.all_gather_object(res, obj)
+        return res
+
+    t_start = time.perf_counter()
+    cfg = PRESETS["llama-3.1-8b"]
+    configs = grid()
+    if args.steps:
+        configs = [S.LoraConfig(c.id, rank=c.rank, alpha=c.alpha, batch_size=c.batch_size,
+                                learning_rate=c.learning_rate, seq_len=c.seq_len, train_steps=args.steps)
+                   for c in configs]
+    by_id = {c.id: c for c in configs}
+    half = ACT_BYTES_PER_TOKEN / 2 / 2
+    model = S.model_spec_from_config(cfg, c_prec=2, act_coeffs=(0.0, half, half), state_bytes=S.STATE_BYTES_PLORA)
+    pool = S.GpuPool(args.gpus, int(args.mem_gb * 1e9), load_factor=0.9)
+
+    cal = calibrate(configs, by_id, model, pool, args.profile_steps) if rank == 0 else None
+    cal = gather(cal)[0]
+    b1, m1 = cal["base_s"], cal["marginal_s"]
     tm = S.TimeModel(coeffs={d: (b1 * d, m1 * d) for d in (1, 2, 4, 8) if d <= args.gpus},
-                     token_weight=best.token_weight)
-    print(f"calibrated: base {b1:.4f} s, marginal {m1:.3e} s/load, token_weight {best.token_weight}, "
-          f"rel rmse {best.fit_rel_rmse[1]:.3f}", flush=True)
-
-    # 3. plan (reference DTM, and the B200 load-balancing extension)
+                     token_weight=cal["token_weight"])
+    if rank == 0:
+        print(f"calibrated: base {b1:.4f} s, marginal {m1:.3e} s/load, token_weight {cal['token_weight']}, "
+              f"rel rmse {cal['rel_rmse']:.3f}", flush=True)
     mem = S.MemoryContext(model, pool, configs)
-    queue_ref = S.plan_jobs(args.gpus, configs, tm, mem)
-    queue = S.plan_jobs(args.gpus, configs, tm, mem, balance=True)
-    pl = S.place(queue, args.gpus)
-    qmin = S.min_gpu_queue(configs, args.gpus, tm, mem)
-    qmax = S.max_gpu_queue(configs, args.gpus, tm, mem)
-    pred = {"planned_balanced": pl.makespan, "planned_reference_dtm": S.place(queue_ref, args.gpus).makespan,
-            "min_gpu": S.place(qmin, args.gpus).makespan,
-            "max_gpu_no_tp_speedup": S.place(qmax, args.gpus).makespan}
-    print("predicted makespans (s):", {k: round(v, 1) for k, v in pred.items()}, flush=True)
-    print("jobs (balanced):", [(len(j.configs), j.degree) for j in queue.jobs()], flush=True)
-    print("jobs (reference DTM):", [(len(j.configs), j.degree) for j in queue_ref.jobs()], flush=True)
-
-    # 4. execute (measured steps, scaled to train_steps): the balanced plan, the reference-DTM
-    # plan and the Min-GPU baseline all run through the engine
-    def run(q):
-        rep = execute(q, configs, args.gpus, steps_override=args.steps_measured)
-        busy = {}
-        for r in rep["records"]:
-            busy[r.device] = busy.get(r.device, 0.0) + r.iter_time_s * max(by_id[c].train_steps for c in r.configs)
-        return max(busy.values()), busy, rep
-    measured, busy, rep = run(queue)
-    measured_ref, _, _ = run(queue_ref)
-    measured_min, _, _ = run(qmin)
-    print(f"measured makespans (s): balanced {measured:.1f}, reference DTM {measured_ref:.1f}, "
-          f"min-GPU {measured_min:.1f}", flush=True)
-    # min-GPU baseline measured the same way would run 64 single-config jobs; use its calibrated prediction
-    out = {"configs": len(configs), "gpus": args.gpus, "jobs": len(queue.jobs()),
-           "measured_makespan_s": {"planned_balanced": measured, "planned_reference_dtm": measured_ref,
-                                   "min_gpu": measured_min},
-           "measured_busy_s": busy, "predicted_makespan_s": pred,
-           "speedup_vs_min_gpu_measured": measured_min / measured,
-           "profiles": [dict(degree=p.parallelism_degree, ranks=list(p.packed_ranks), batch_sizes=list(p.packed_batch_sizes),
-                             seq_len=p.seq_len, iter_time_s=p.iter_time_s) for p in profiles + rep["profiles"]],
-           "time_model": {"base_s": b1, "marginal_s": m1, "token_weight": best.token_weight,
-                          "rel_rmse": best.fit_rel_rmse[1]},
-           "queue": json.loads(S.serialize_queue(queue)), "wall_s": time.perf_counter() - t_start,
-           "note": ("each job executed for --steps-measured steps on its placed device; with one physical GPU the "
-                    "8 devices' jobs run back to back and per-device busy time is summed separately")}
-    os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    with open(args.out, "w") as f:
-        json.dump(out, f, indent=1)
-    print(json.dumps({k: out[k] for k in ("jobs", "measured_makespan_s", "predicted_makespan_s",
-                                          "speedup_vs_min_gpu_measured", "wall_s")}), flush=True)
+    queues = {"balanced": S.plan_jobs(args.gpus, configs, tm, mem, balance=True),
+              "reference": S.plan_jobs(args.gpus, configs, tm, mem),
+              "min": S.min_gpu_queue(configs, args.gpus, tm, mem)}
+    out = {"configs": len(configs), "gpus": args.gpus, "processes": world, "time_model": cal, "plans": {}}
+    for name in args.plans.split(","):
+        q = queues[name]
+        pred = S.place(q, args.gpus).makespan
+        rep = execute(q, configs, args.gpus, rank=rank, world=world, all_gather=gather, pool=pool)
+        bound = S.ar_bound(rep["trace"])
+        out["plans"][name] = {
+            "jobs": len(q.jobs()), "degrees": sorted({j.degree for j in q.jobs()}),
+            "predicted_makespan_s": pred, "measured_makespan_s": rep["makespan_s"], "clock": rep["clock"],
+            "violations": rep["violations"], "ar_bound": bound.bound,
+            "busy_s": rep["busy_s"],
+            "trace": [dict(job=j.job_id, configs=len(j.configs), degree=j.degree, devices=list(j.devices),
+                           start_s=round(j.start_s, 3), duration_s=round(j.duration_s, 3),
+                           predicted_s=round(j.predicted_s, 3)) for j in rep["trace"].jobs]}
+        if rank == 0:
+            print(f"{name}: {len(q.jobs())} jobs, predicted {pred:.1f} s, measured {rep['makespan_s']:.1f} s "
+                  f"({rep['clock']} clock), violations {len(rep['violations'])}", flush=True)
+    if rank == 0:
+        out["wall_s"] = time.perf_counter() - t_start
+        if "balanced" in out["plans"] and "min" in out["plans"]:
+            out["speedup_vs_min_gpu_measured"] = (out["plans"]["min"]["measured_makespan_s"]
+                                                  / out["plans"]["balanced"]["measured_makespan_s"])
+        os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+        with open(args.out, "w") as f:
+            json.dump(out, f, indent=1)
+        print(json.dumps({k: {kk: v[kk] for kk in ("jobs", "predicted_makespan_s", "measured_makespan_s", "clock",
+                                                     "violations")} for k, v in out["plans"].items()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
