@@ -1,8 +1,9 @@
 """Tensor-parallel packed LoRA (config C4's path) on ONE B200: a TP group of g ranks
 runs as g threads sharing the GPU (tp.ThreadComm, each rank on its own stream, the
 same sharded kernels and all-reduce placement the NCCL path uses).  The sharded
-job must reproduce the unsharded packed trainer (itself parity-pinned to the fp64
-oracle in test_gpu_model.py):
+job is compared directly with the fp64 oracle decoder (oracle/model_oracle.py: every
+LoRA linear is the reference's packed_forward / packed_backward restated), on the
+unsharded model's weights, at the C1 tier of test_gpu_model.py:
 
   per-adapter loss                     |d| / |ref| <= 1e-2
   per-(layer, target, factor, adapter) gradient, shards reassembled:
@@ -13,6 +14,7 @@ oracle in test_gpu_model.py):
 import pytest
 import torch
 
+from oracle.model_oracle import from_trainer, oracle_step
 from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
 from paper_2508_02932_b200.tp import TPShard, run_threaded
 
@@ -38,6 +40,22 @@ def _grads(tr):
     return out
 
 
+def oracle_reference(tr, tokens):
+    """fp64 oracle losses and per-(layer, target, factor, adapter) LoRA gradients of the
+    unsharded model ``tr`` (its weights only: nothing of ``tr`` runs), keyed and laid out
+    like _grads (A_i [h_in][r], B_i^T [h_out][r])."""
+    base, adapters = from_trainer(tr)
+    n_lab = [sp.batch * (tr.s - 1) for sp in tr.specs]
+    losses, grads, _ = oracle_step(tr.cfg, base, adapters, [sp.alpha for sp in tr.specs], tr.meta.row_offsets,
+                                   tokens.cpu(), tr.s, tr.cos.double().cpu(), tr.sin.double().cpu(), n_lab)
+    out = {}
+    for (layer, tname), (dd, du) in grads.items():
+        for i in range(tr.meta.n_adapters):
+            out[(layer, tname, "A", i)] = dd[i].float()
+            out[(layer, tname, "B", i)] = du[i].t().float()
+    return losses.double(), out
+
+
 def _masters(tr):
     bank = tr.bank
     return {(layer, t.name, kind, i): bank.block(bank.P, layer, t.name, kind, i).cpu().clone()
@@ -49,17 +67,17 @@ def _masters(tr):
                                                     ("tiny-qwen", 2, True, False, False),
                                                     ("tiny-qwen", 2, False, True, False),
                                                     ("tiny", 4, False, True, False), ("tiny-qwen", 2, True, True, True)])
-def test_tp_matches_unsharded(preset, g, sp, keep, fused):
+def test_tp_matches_oracle(preset, g, sp, keep, fused):
     """sp: Megatron sequence parallelism (token-sharded residual stream; g = 2 cuts the
     pair-tile list exactly at the shard boundaries -> per-shard reduces overlapping the
     GEMM; g = 4 does not -> one reduce-scatter); sp = False: all-reduce chunks.
     keep = False: the normed inputs are re-gathered in the backward on the side stream.
     fused: the row-parallel GEMMs reduce their tiles straight into the owning rank's
     buffer (TMA reduce-add into peer memory -- here the other threads' buffers)."""
-    ref = _make(preset)
+    ref = _make(preset)                      # unsharded weights for the oracle (not run)
     tokens = ref.synthetic_tokens().cuda()
-    ref_losses = ref.forward_backward(tokens).double().cpu()
-    ref_grads = _grads(ref)
+    ref_losses, ref_grads = oracle_reference(ref, tokens)
+    del ref
 
     def rank_fn(comm):
         tr = _make(preset, tp=comm, sp=sp, save_normed=keep, fused=fused)

@@ -2,9 +2,9 @@
 through torch.distributed (tp.DistComm) -- the code path a real TP job uses, with the
 gloo backend standing in for NCCL (NCCL refuses two ranks on one device; gloo moves
 CUDA tensors through the host).  Each rank builds its Megatron shard, runs one
-forward + backward and a fused AdamW step; the parent compares with the unsharded
-trainer (same tolerances as test_gpu_tp.py) and checks the replicated factors are
-bit-identical across the two processes."""
+forward + backward and a fused AdamW step; the parent compares with the fp64 oracle
+decoder on the unsharded model's weights (same tolerances as test_gpu_tp.py) and
+checks the replicated factors are bit-identical across the two processes."""
 
 import os
 import socket
@@ -16,6 +16,7 @@ import torch.multiprocessing as mp
 
 from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
 from paper_2508_02932_b200.tp import DistComm, TPShard
+from tests.test_gpu_tp import oracle_reference
 
 pytestmark = pytest.mark.gpu
 
@@ -61,10 +62,9 @@ def test_tp2_two_processes_gloo(keep, fused):
     """(The fused peer-memory path is not covered here: torch symmetric memory refuses two
     ranks on one device -- "allocations from overlapping devices"; test_gpu_tp.py covers
     it with thread-emulated ranks.)"""
-    ref = _make()
+    ref = _make()                            # unsharded weights for the oracle (not run)
     tokens = ref.synthetic_tokens().cuda()
-    ref_losses = ref.forward_backward(tokens).double().cpu()
-    ref_grads = _grads(ref)
+    ref_losses, ref_grads = oracle_reference(ref, tokens)
     del ref
     torch.cuda.empty_cache()
     mgr = mp.Manager()
