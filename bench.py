@@ -461,6 +461,8 @@ def main() -> None:
     launches = ops.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     kstats = timer.summary()
+    if os.environ.get("PLORA_RECORDS_OUT") and rank == 0:   # per-launch records for tools/dram_by_shape.py
+        Path(os.environ["PLORA_RECORDS_OUT"]).write_text(json.dumps(timer.dump()))
     ms_max = max_over_ranks(ms)
     # tokens processed by the whole job: a TP group's ranks share one job's tokens
     tokens_all = sum_over_ranks(float(T) if (tp == 1 or rank % tp == 0) else 0.0)

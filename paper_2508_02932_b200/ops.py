@@ -25,34 +25,44 @@ class KernelTimer:
 
     While active, packed linears are issued as their component launches
     (shrink / segment reductions / GEMM) with events recorded on the launching
-    stream around each, together with that launch's ALGORITHMIC flops and bytes."""
+    stream around each, together with that launch's ALGORITHMIC flops and HBM bytes
+    (``nbytes``: the roofline bytes of the HBM-bound kernels; ``algo_bytes``: operand +
+    output bytes of every launch, the denominator of ncu's DRAM-traffic ratio)."""
 
     def __init__(self):
-        self.records: list[tuple[str, torch.cuda.Event, torch.cuda.Event, float, float]] = []
+        self.records: list = []
 
     def start(self):
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         return e
 
-    def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0, detail: str | None = None):
+    def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0, detail: str | None = None,
+             algo_bytes: float | None = None):
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
-        self.records.append((kind, e0, e1, flops, nbytes))
-        if detail is not None:
-            self.records.append((f"{kind}[{detail}]", e0, e1, flops, nbytes))
+        self.records.append((kind, e0, e1, flops, nbytes, detail, nbytes if algo_bytes is None else algo_bytes))
 
     def summary(self) -> dict:
         """Per kernel class (and per GEMM shape, keys 'gemm[N..K..]'): launches, ms, flops, bytes."""
         torch.cuda.synchronize()
         out: dict = {}
-        for kind, e0, e1, fl, nb in self.records:
-            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
-            d["launches"] += 1
-            d["ms"] += e0.elapsed_time(e1)
-            d["flops"] += fl
-            d["bytes"] += nb
+        for kind, e0, e1, fl, nb, detail, _ in self.records:
+            ms = e0.elapsed_time(e1)
+            keys = [kind] + ([f"{kind}[{detail}]"] if detail is not None and kind == "gemm" else [])
+            for key in keys:
+                d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+                d["launches"] += 1
+                d["ms"] += ms
+                d["flops"] += fl
+                d["bytes"] += nb
         return out
+
+    def dump(self) -> list:
+        """One entry per timed libplora launch, in issue order (for matching an ncu launch list)."""
+        torch.cuda.synchronize()
+        return [{"kind": k, "detail": d, "ms": round(e0.elapsed_time(e1), 4), "flops": fl, "hbm_bytes": nb,
+                 "algo_bytes": ab} for k, e0, e1, fl, nb, d, ab in self.records]
 
 
 _TIMER: KernelTimer | None = None
@@ -127,7 +137,8 @@ def gemm(a: torch.Tensor, w: torch.Tensor, w_kmajor: bool = True, out: torch.Ten
         out.stride(0), _need(residual, "residual", allow_none=True)), "plora_gemm_bf16")
     _LAUNCHES[0] += 1
     if t is not None:
-        _TIMER.stop("gemm", t, flops=2.0 * M * N * K, detail=f"N{N}K{K}{'k' if w_kmajor else 'mn'}")
+        _TIMER.stop("gemm", t, flops=2.0 * M * N * K, detail=f"N{N}K{K}{'k' if w_kmajor else 'mn'}",
+                    algo_bytes=2.0 * (M * K + N * K + M * N))
     return out
 
 
@@ -170,7 +181,7 @@ def shrink(meta: PackMeta, p: torch.Tensor, l_sh: torch.Tensor, out: torch.Tenso
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)
-        _TIMER.stop("shrink", t, flops=2.0 * K * tr, nbytes=2.0 * T * K + 2.0 * K * R + 2.0 * tr)
+        _TIMER.stop("shrink", t, flops=2.0 * K * tr, nbytes=2.0 * T * K + 2.0 * K * R + 2.0 * tr, detail=f"K{K}")
     return out
 
 
@@ -186,7 +197,8 @@ def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) ->
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)
-        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr, nbytes=2.0 * T * Mdim + 2.0 * tr + 4.0 * Mdim * R)
+        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr, nbytes=2.0 * T * Mdim + 2.0 * tr + 4.0 * Mdim * R,
+                    detail=f"M{Mdim}")
     return g
 
 
@@ -211,7 +223,8 @@ def shrink_multi(meta: PackMeta, p: torch.Tensor, l_shs, outs) -> list:
     if t is not None:
         tr, R = _lora_work(meta)
         m = len(outs)
-        _TIMER.stop("shrink", t, flops=2.0 * K * tr * m, nbytes=2.0 * T * K + m * (2.0 * K * R + 2.0 * tr))
+        _TIMER.stop("shrink", t, flops=2.0 * K * tr * m, nbytes=2.0 * T * K + m * (2.0 * K * R + 2.0 * tr),
+                    detail=f"K{K}x{m}")
     return outs
 
 
@@ -231,7 +244,8 @@ def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
     if t is not None:
         tr, R = _lora_work(meta)
         m = len(gs)
-        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr * m, nbytes=2.0 * T * Mdim + m * (2.0 * tr + 4.0 * Mdim * R))
+        _TIMER.stop("segred", t, flops=2.0 * Mdim * tr * m, nbytes=2.0 * T * Mdim + m * (2.0 * tr + 4.0 * Mdim * R),
+                    detail=f"M{Mdim}x{m}")
     return gs
 
 
@@ -266,7 +280,8 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
     if t is not None:
         tr, R = _lora_work(meta)
         _TIMER.stop("gemm", t, flops=sum(2.0 * T * d * k + 2.0 * k * tr for k in ks),
-                    detail="grp" + "+".join(f"N{k}" for k in ks) + f"K{d}{'k' if w_kmajor else 'mn'}")
+                    detail="grp" + "+".join(f"N{k}" for k in ks) + f"K{d}{'k' if w_kmajor else 'mn'}",
+                    algo_bytes=2.0 * (T * d + sum(k * d + T * k + T * meta.rpad64 for k in ks)))
     return ys
 
 
@@ -296,7 +311,8 @@ def linear_gate_up_swiglu(meta: PackMeta, x: torch.Tensor, w_gate: torch.Tensor,
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)
-        _TIMER.stop("gemm", t, flops=2 * (2.0 * T * d * ffn + 2.0 * ffn * tr), detail=f"gateup+swiglu N{ffn}K{d}k")
+        _TIMER.stop("gemm", t, flops=2 * (2.0 * T * d * ffn + 2.0 * ffn * tr), detail=f"gateup+swiglu N{ffn}K{d}k",
+                    algo_bytes=2.0 * (T * d + 2 * ffn * d + 3 * T * ffn + 2 * T * meta.rpad64))
     return g, u, act
 
 
@@ -326,7 +342,8 @@ def linear_dx_group(meta: PackMeta, dys, ws, a_shs, dhs, d: int, w_kmajor: bool 
     if t is not None:
         tr, R = _lora_work(meta)
         _TIMER.stop("gemm", t, flops=sum(2.0 * T * d * k + 2.0 * d * tr for k in ks),
-                    detail="grp" + "+".join(f"K{k}" for k in ks) + f"N{d}{'mn' if w_kmajor else 'k'}")
+                    detail="grp" + "+".join(f"K{k}" for k in ks) + f"N{d}{'mn' if w_kmajor else 'k'}",
+                    algo_bytes=2.0 * (T * d + sum(T * k + k * d + T * meta.rpad64 for k in ks)))
     return dx_out
 
 
@@ -350,7 +367,9 @@ def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bo
     _LAUNCHES[0] += 1
     if t is not None:
         tr, R = _lora_work(meta)
-        _TIMER.stop("gemm", t, flops=2.0 * T * d * k + 2.0 * k * tr, detail=f"N{k}K{d}{'k' if w_kmajor else 'mn'}")
+        _TIMER.stop("gemm", t, flops=2.0 * T * d * k + 2.0 * k * tr, detail=f"N{k}K{d}{'k' if w_kmajor else 'mn'}",
+                    algo_bytes=2.0 * (T * d + k * d + T * k + T * meta.rpad64) + (2.0 * T * k if residual is not None
+                                                                                 else 0.0))
     return y_out
 
 
@@ -411,7 +430,8 @@ def adamw(chunks: torch.Tensor, param: torch.Tensor, grad: torch.Tensor, exp_avg
         "plora_adamw")
     if t is not None:
         # 30 B per trainable parameter: read p,g,m,v (16) + write p,m,v (12) + bf16 shadow (2)
-        _TIMER.stop("adamw", t, nbytes=30.0 * (algo_params if algo_params is not None else param.numel()))
+        _TIMER.stop("adamw", t, nbytes=30.0 * (algo_params if algo_params is not None else param.numel()),
+                    detail="K7")
 
 
 # ------------------------------------------------------------------ torch training op

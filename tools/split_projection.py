@@ -1,0 +1,86 @@
+"""Planner-split scaling on ONE GPU: every rank's packed job of the N-GPU split
+(sweep/jobsplit.py, the split bench.py --gpus N runs) trained here one after the other,
+device-timed like bench.py.  Ranks of a real N-GPU run are independent processes on
+their own GPUs with no data-path collective, so the N-GPU step time is the slowest
+rank's: projected tokens/s = total tokens / max_r(step time of rank r).  A projection,
+not a bench value (one GPU, ranks timed sequentially, no cross-rank interference).
+
+  python tools/split_projection.py [--config llama-3.1-8b] [--gpus 2,4,8] [--steps 5] [--warmup 2]
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
+import torch  # noqa: E402
+
+from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters  # noqa: E402
+from paper_2508_02932_b200.sweep.engine import _base  # noqa: E402
+from paper_2508_02932_b200.sweep.jobsplit import split_adapters  # noqa: E402
+
+
+def time_job(cfg_name, idx, steps, warmup):
+    cfg = PRESETS[cfg_name]
+    specs, s = bench_adapters(cfg_name)
+    sub = [specs[i] for i in idx]
+    tr = PackedLoraTrainer(cfg, sub, s, device="cuda", base=_base(cfg_name, "cuda:0"),
+                           adapter_seeds=[100 + i for i in idx])
+    tok = tr.synthetic_tokens(seeds=[1000 + i for i in idx]).cuda()
+    for _ in range(warmup):
+        tr.step(tok)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        tr.step(tok)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    T = tr.T
+    del tr
+    torch.cuda.empty_cache()
+    return T, ms
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="llama-3.1-8b")
+    ap.add_argument("--gpus", default="1,2,4,8")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    cache = {}
+    out = {"config": args.config, "projection": []}
+    one = None
+    for n in [int(x) for x in args.gpus.split(",")]:
+        sp = split_adapters(args.config, n)
+        ranks = []
+        for r, idx in enumerate(sp.adapters):
+            key = tuple(idx)
+            if key not in cache:
+                cache[key] = time_job(args.config, list(idx), args.steps, args.warmup)
+            T, ms = cache[key]
+            ranks.append({"rank": r, "adapters": list(idx), "tokens": T, "ms_per_step": round(ms, 2),
+                          "tokens_per_s": round(T / ms * 1000, 1)})
+        total = sum(x["tokens"] for x in ranks)
+        step = max(x["ms_per_step"] for x in ranks)
+        v = total / step * 1000
+        if n == 1:
+            one = v
+        row = {"gpus": n, "split": sp.describe(), "projected_tokens_per_s": round(v, 1),
+               "slowest_rank_ms": step, "efficiency_vs_1gpu": round(v / (n * one), 4) if one else None,
+               "ranks": ranks}
+        out["projection"].append(row)
+        print(json.dumps({k: row[k] for k in ("gpus", "split", "projected_tokens_per_s", "slowest_rank_ms",
+                                                "efficiency_vs_1gpu")}), flush=True)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
