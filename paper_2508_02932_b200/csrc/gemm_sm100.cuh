@@ -58,7 +58,6 @@ struct __align__(64) GemmArgs {
   int32_t mt_per;    // SEGRED: ceil(M/128)
   int32_t has_lora;
   int32_t nb;        // 64-column rank blocks
-  int32_t debug;     // bit 0: skip epilogue stores (profiling experiments only)
   int32_t accumulate;  // pair kernel: Y += result (TMA reduce-add) instead of Y = result
   // Multi-target SHRINK / SEGRED (n_multi > 1, rank <= 64): targets j = 0..n_multi-1 share
   // the A operand (the same X), each with its own 64-column B operand (tmB, tmB2, tmB3)
@@ -765,11 +764,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * Cfg::kStageBytes;
           uint8_t* sB = sA + Cfg::kABytes;
-          if (args.debug & 2) {  // profiling experiment: no operand traffic
-            if (leader) mbar_arrive(&full_bar[stage]);
-            if (++stage == S) { stage = 0; phase ^= 1; }
-            continue;
-          }
           const bool paired_lora = EPI == EPI_SWIGLU && b >= t.n_main;   // A + one B chunk
           if (leader) mbar_expect_tx(&full_bar[stage], paired_lora ? 2 * (Cfg::kABytes + 16384) : 2 * Cfg::kStageBytes);
           const uint32_t fb = peer_masked(&full_bar[stage]);
@@ -946,8 +940,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * Cfg::kBN + (static_cast<uint32_t>(quarter * 32) << 16);
       const int c0 = chalf * kChunks;
-      const bool skip = (args.debug & 1) != 0;
-      const bool store = !skip && !(args.debug & 4) && m_len > 0;   // bit 2: TMEM drain only (experiment)
+      const bool store = m_len > 0;
       PairOut po;
       po.tm = seg_map(&args.tmY, p.tmY2, t.seg);
       po.out = static_cast<__nv_bfloat16*>(p.seg_out[t.seg]);
@@ -956,7 +949,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
       po.accumulate = args.accumulate;
       po.bias = static_cast<const __nv_bfloat16*>(p.seg_bias[t.seg]);
       uint32_t pk[kParked > 0 ? kParked : 1][16];
-      if (!skip) {
+      {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tb + c0 * 32, r);
 #pragma unroll

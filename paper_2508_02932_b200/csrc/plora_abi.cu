@@ -73,8 +73,56 @@ static EncodeTiledFn get_encode() {
 #define PLORA_LOAD_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B   // operand loads (build-time knob)
 #endif
 
+// Tensor-map cache: a CUtensorMap is a pure function of (kind, base, extents, pitch, box),
+// and the caching allocators behind the callers hand the same buffers back step after
+// step, so each map is encoded once per process (per-launch host work matters when
+// tokens per GPU shrink under the planner split).  Bounded; thread-safe.
+struct MapKey {
+  uint64_t v[7];
+  bool operator==(const MapKey& o) const { return memcmp(v, o.v, sizeof(v)) == 0; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t x : k.v) h = (h ^ x) * 1099511628211ull;
+    return static_cast<size_t>(h);
+  }
+};
+static std::mutex g_map_mu;
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+template <typename F>
+static int cached_map(CUtensorMap* m, const MapKey& key, F&& encode) {
+  {
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *m = it->second;
+      return 0;
+    }
+  }
+  int rc = encode(m);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  if (g_maps.size() >= 8192) g_maps.clear();
+  g_maps.emplace(key, *m);
+  return 0;
+}
+
+static int make_map_2d_enc(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer);
+
 static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+  const MapKey key{{1, reinterpret_cast<uint64_t>(base), inner, outer, pitch_elems, box_inner,
+                    static_cast<uint64_t>(box_outer)}};
+  return cached_map(m, key, [&](CUtensorMap* mm) {
+    return make_map_2d_enc(mm, base, inner, outer, pitch_elems, box_inner, box_outer);
+  });
+}
+
+static int make_map_2d_enc(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail("tensor base not 16-byte aligned");
@@ -94,7 +142,14 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
 }
 
 // 2D bf16 output tensor for the TMA-store epilogue: 32x32 boxes, 64-byte swizzle.
+static int make_map_out_enc(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_elems);
+
 static int make_map_out(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_elems) {
+  const MapKey key{{2, reinterpret_cast<uint64_t>(base), cols, rows, pitch_elems, 32, 32}};
+  return cached_map(m, key, [&](CUtensorMap* mm) { return make_map_out_enc(mm, base, cols, rows, pitch_elems); });
+}
+
+static int make_map_out_enc(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_elems) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (reinterpret_cast<uintptr_t>(base) % 16 || (pitch_elems * 2) % 16)
@@ -111,8 +166,17 @@ static int make_map_out(CUtensorMap* m, const void* base, uint64_t cols, uint64_
 }
 
 // 3D bf16 tensor [n][mid][inner] (dense), box {box_inner, box_mid, 1}.
+static int make_map_3d_enc(CUtensorMap* m, const void* base, uint64_t inner, uint64_t mid, uint64_t n,
+                           uint32_t box_inner, uint32_t box_mid);
+
 static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t mid, uint64_t n,
                        uint32_t box_inner, uint32_t box_mid) {
+  const MapKey key{{3, reinterpret_cast<uint64_t>(base), inner, mid, n, box_inner, box_mid}};
+  return cached_map(m, key, [&](CUtensorMap* mm) { return make_map_3d_enc(mm, base, inner, mid, n, box_inner, box_mid); });
+}
+
+static int make_map_3d_enc(CUtensorMap* m, const void* base, uint64_t inner, uint64_t mid, uint64_t n,
+                           uint32_t box_inner, uint32_t box_mid) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail("tensor base not 16-byte aligned");
@@ -170,15 +234,21 @@ static int launch(const GemmArgs& args, cudaStream_t stream) {
 
 static int pick_bn(int64_t N) { return N >= 256 ? 256 : (N > 64 ? 128 : 64); }
 
-static int g_debug_flags = [] {
-  const char* e = getenv("PLORA_DEBUG_FLAGS");
-  return e ? atoi(e) : 0;
-}();
-
-static bool g_pair_enabled = [] {
-  const char* e = getenv("PLORA_GEMM_PAIR");
-  return !(e && e[0] == '0');
-}();
+// Tile-shape policy of the base GEMMs.  Build-time constants (-D overrides for
+// experiments, tools/build_variant.sh); the values are the measured optima of round 1
+// (DESIGN.md section 6).
+#ifndef PLORA_PAIR_NB1_MAXK
+#define PLORA_PAIR_NB1_MAXK 1024   // K at or below which 256x256 double-buffered pair tiles are used
+#endif
+#ifndef PLORA_PAIR512_MIN_N
+#define PLORA_PAIR512_MIN_N 2048   // N at which the 256x512 pair tile is used
+#endif
+#ifndef PLORA_PAIR_BAND
+#define PLORA_PAIR_BAND (-8)       // pair-GEMM raster: N-bands of 8 column tiles
+#endif
+#ifndef PLORA_GROUP_MIN_N
+#define PLORA_GROUP_MIN_N 64       // narrowest segment of a grouped (multi-target) pair launch
+#endif
 
 template <bool B_MN, int NB, int EPI = EPI_STORE>
 static int launch_pair(const PairArgs& args, cudaStream_t stream) {
@@ -194,25 +264,15 @@ static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   return 0;
 }
 
-static int g_pair_nb1_max_k = [] {   // K at or below which 256x256 double-buffered tiles are used
-  const char* e = getenv("PLORA_PAIR_NB1_MAXK");
-  return e ? atoi(e) : 1024;   // C4 TP shards (o: K = 640, q/k/v dX: K = 896): ~1% per layer
-}();
-
-static int g_pair_nb_min_n = [] {   // N at which the 256x512 pair tile is used
-  const char* e = getenv("PLORA_PAIR512_MIN_N");
-  return e ? atoi(e) : 2048;
-}();
-
+// 256x256 tiles at K <= 1024: C4 TP shards (o: K = 640, q/k/v dX: K = 896), ~1% per layer.
+static constexpr int g_pair_nb1_max_k = PLORA_PAIR_NB1_MAXK;
+static constexpr int g_pair_nb_min_n = PLORA_PAIR512_MIN_N;
 // Tile raster of the pair GEMM: N-bands of 8 column tiles (4096 output columns at
 // NB = 2), row groups stepping inside a band, so every A row block is consumed by 8
 // concurrently running clusters.  Measured on the C3 step (same box, alternating runs):
 // DRAM reads per GEMM -27%, SM clock under the power cap +45 MHz, +2.6% tokens/s vs
-// 8-row-group M-bands (the previous raster, PLORA_PAIR_BAND=0 / >0 to restore).
-static int g_pair_band = [] {
-  const char* e = getenv("PLORA_PAIR_BAND");
-  return e ? atoi(e) : -8;
-}();
+// 8-row-group M-bands (the previous raster, PLORA_PAIR_BAND >= 0).
+static constexpr int g_pair_band = PLORA_PAIR_BAND;
 
 // One segment of a (segmented) pair GEMM; see PairArgs in gemm_sm100.cuh.
 struct PairSeg {
@@ -318,7 +378,6 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
                                    cudaMemcpyDeviceToDevice, st));
     a.accumulate = 1;
   }
-  a.debug = g_debug_flags;
   pa.band = g_pair_band;
   if (paired) return launch_pair<false, 2, EPI_SWIGLU>(pa, st);
   if (NB == 2) return w_kmajor ? launch_pair<false, 2>(pa, st) : launch_pair<true, 2>(pa, st);
@@ -342,7 +401,7 @@ static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_
   if (K % 8 || N % 8 || ldy % 8) return fail("gemm: K, N and ldy must be multiples of 8");
   if (reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16))
     return fail("gemm: output/residual must be 16-byte aligned");
-  if (g_pair_enabled && N >= 256 && (pack == nullptr || pack->d_ptiles != nullptr || pack->n_ptiles == 0))
+  if (N >= 256 && (pack == nullptr || pack->d_ptiles != nullptr || pack->n_ptiles == 0))
     return run_gemm_pair(st, pack, M, N, K, A, W, w_kmajor, H, L, Y, ldy, residual, bias);
   const int BN = pick_bn(N);
   GemmArgs a;
@@ -399,11 +458,6 @@ static int run_shrink(cudaStream_t st, const plora_pack_t* pack, int64_t K, cons
   a.ldo = R64;
   return launch<64, MODE_SHRINK, true>(a, st);
 }
-
-static bool g_segred_lpt = [] {
-  const char* e = getenv("PLORA_SEGRED_LPT");
-  return !(e && e[0] == '0');
-}();
 
 // LPT schedule for the segment reductions: tile (adapter a, m-tile, n-tile) costs
 // ceil(T_a / 64) K-blocks + a fixed epilogue/fill overhead; tiles are taken in
@@ -494,7 +548,7 @@ static int run_segred(cudaStream_t st, const plora_pack_t* pack, int64_t Mdim, c
   a.M = static_cast<int>(Mdim);
   a.N = static_cast<int>(R64);
   a.out = G;
-  if (pack->h_row_off != nullptr && g_segred_lpt) {
+  if (pack->h_row_off != nullptr) {
     SegSched sched;
     if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched)) return launch_segred_lpt<64>(a, sched, st);
   }
@@ -555,7 +609,7 @@ static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t M
   a.out2 = n_multi > 1 ? G[1] : nullptr;
   a.out3 = n_multi > 2 ? G[2] : nullptr;
   a.n_multi = n_multi;
-  if (pack->h_row_off != nullptr && g_segred_lpt) {
+  if (pack->h_row_off != nullptr) {
     SegSched sched;
     if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched))
       return n_multi == 3 ? launch_segred_lpt<192>(a, sched, st) : launch_segred_lpt<128>(a, sched, st);
@@ -665,13 +719,12 @@ int plora_linear_expand(void* stream, const plora_pack_t* pack, const void* X, i
                   Hs, Bt_sh, Y, ldy, residual);
 }
 
-static int g_group_min_n = [] {   // narrowest grouped segment (narrower: separate launches)
-  const char* e = getenv("PLORA_GROUP_MIN_N");
-  return e ? atoi(e) : 64;   // narrow TP-shard k/v (N = 128) ride the grouped launch: ~1% per C4 layer
-}();
+// narrowest grouped segment (narrower: separate launches); narrow TP-shard k/v (N = 128)
+// ride the grouped launch: ~1% per C4 layer
+static constexpr int g_group_min_n = PLORA_GROUP_MIN_N;
 
 static bool group_pair_ok(const plora_pack_t* pack, int n, const int64_t* N) {
-  if (!g_pair_enabled || (pack->d_ptiles == nullptr && pack->n_ptiles != 0)) return false;
+  if (pack->d_ptiles == nullptr && pack->n_ptiles != 0) return false;
   int64_t widest = 0;
   for (int j = 0; j < n; ++j) {
     if (N[j] < g_group_min_n) return false;
@@ -711,7 +764,7 @@ int plora_linear_gate_up_swiglu(void* stream, const plora_pack_t* pack, const vo
   if (!g || !u || !act) return fail("gate_up_swiglu: g, u and act are required");
   const int64_t T = pack->total_tokens;
   if (T <= 0) return 0;
-  if (!g_pair_enabled || (pack->d_ptiles == nullptr && pack->n_ptiles != 0) || ffn < 256)
+  if ((pack->d_ptiles == nullptr && pack->n_ptiles != 0) || ffn < 256)
     return fail("gate_up_swiglu: needs the CTA-pair GEMM and ffn >= 256");
   PairSeg sg[2] = {PairSeg{X, d, W_gate, ffn, Hs_gate, Bt_gate, g, ffn}, PairSeg{X, d, W_up, ffn, Hs_up, Bt_up, u, ffn}};
   return run_pair_segments(static_cast<cudaStream_t>(stream), pack, T, 2, 1, sg, 1, nullptr, act);

@@ -23,7 +23,6 @@ recomputed.
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -211,13 +210,17 @@ class PackedLoraTrainer:
     def __init__(self, cfg: ModelConfig, specs: Sequence[AdapterSpec], seq_len: int, device="cuda",
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
-                 save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool | None = None):
+                 save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool = False,
+                 tp_chunks: int = 4, fuse_swiglu: bool = True):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
         when tp divides T) also shards the residual stream over tokens.
         ``save_normed``: keep the normed layer inputs for the backward (None: when the
-        activation estimate leaves headroom on the device)."""
+        activation estimate leaves headroom on the device).  ``tp_chunks``: token chunks of
+        the TP all-reduce / GEMM overlap; ``tp_fused``: row-parallel GEMMs reduce into the
+        owner's buffer over peer memory (opt-in, unmeasured on NVLink); ``fuse_swiglu``:
+        gate/up GEMM with the SwiGLU forward in its epilogue."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -248,7 +251,7 @@ class PackedLoraTrainer:
                                 a_scale=a_scale, b_std=b_std, full_targets=cfg.targets(),
                                 shard=self.shard if self.tp is not None else None)
         self.cos, self.sin = rope_tables(cfg, seq_len, self.device)
-        self.ce_chunk = int(os.environ.get("PLORA_CE_CHUNK", ce_chunk))   # tokens per lm_head + CE chunk
+        self.ce_chunk = int(ce_chunk)   # tokens per lm_head + CE chunk
         # per-token adapter id and the CE weight 1/n_i (labels exist for s-1 tokens per sequence)
         ta = torch.from_numpy(self.meta.token_adapter.astype("int64")).to(self.device)
         n_lab = torch.tensor([max(sp.batch * (seq_len - 1), 1) for sp in specs], dtype=torch.float32,
@@ -259,15 +262,13 @@ class PackedLoraTrainer:
         self.ce_weight = torch.where(self.has_label, 1.0 / n_lab[ta], torch.zeros((), device=self.device))
         self.losses = torch.zeros(self.meta.n_adapters, dtype=torch.float32, device=self.device)
         self.save_normed = self._fits_saved_norms() if save_normed is None else bool(save_normed)
-        self.tp_chunks = int(os.environ.get("PLORA_TP_CHUNKS", "4"))   # TP all-reduce / GEMM overlap depth
+        self.tp_chunks = int(tp_chunks)   # TP all-reduce / GEMM overlap depth
         self._side = None
         # fused GEMM + reduce onto owners through peer memory (opt-in, see _fused_reduce)
-        if tp_fused is None:
-            tp_fused = os.environ.get("PLORA_TP_FUSED", "0") == "1"
         self.tp_fused = bool(tp_fused and self.sp and getattr(self.tp, "supports_peer_memory", False))
         self._peer = {}
         # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
-        self._fuse_swiglu = self.targets[4].h_out >= 256 and os.environ.get("PLORA_FUSE_SWIGLU", "1") != "0"
+        self._fuse_swiglu = self.targets[4].h_out >= 256 and fuse_swiglu
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
@@ -476,7 +477,7 @@ class PackedLoraTrainer:
     def _gather_parts(self, x_s: torch.Tensor):
         """Sequence-parallel forward all-gather of the normed input, overlapped with its
         consumers: the shards are broadcast from their owners on the side stream in the
-        PLORA_TP_CHUNKS launch groups; returns (x_full, [(sub_pack, event)]) so the
+        ``tp_chunks`` launch groups; returns (x_full, [(sub_pack, event)]) so the
         column-parallel kernels of a group start as soon as its rows arrived -- or
         (x_full, None) after a plain all-gather when the tile lists cannot be cut at
         the shard boundaries."""
