@@ -346,6 +346,9 @@ def main() -> None:
     ap.add_argument("--tp-comm", default="torch", choices=["torch", "abi"],
                     help="TP all-reduce through torch.distributed (NCCL) or libplora's C-ABI (plora_tp_*, NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="time the step replayed from one CUDA graph (model.GraphedStep; default)")
+    ap.add_argument("--eager", dest="graph", action="store_false", help="time the eager step instead")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         raise SystemExit(_relaunch(args))
@@ -438,50 +441,78 @@ def main() -> None:
             trainer.step(tokens)
     barrier()
 
-    # ---------------------------------------------------------------- timed region (device)
-    timer = ops.KernelTimer()
-    launches0 = ops.launch_count()
-    profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
-    with ClockSampler(device) as clocks:
+    def timed_region(run, steps, sample_clocks=None):
+        """Device time (ms) of `steps` calls of run() between barriers + synchronize, max
+        over ranks (CUDA events on the launching stream)."""
         barrier()
-        if profile_range:
-            torch.cuda.profiler.start()
-        ops.set_timer(timer)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
-            if trainer is not None:
-                trainer.step(tokens)
+        for _ in range(steps):
+            run()
         e1.record()
-        ops.set_timer(None)
         barrier()
-        if profile_range:
-            torch.cuda.profiler.stop()
-    launches = ops.launch_count() - launches0
-    ms = e0.elapsed_time(e1)
+        return e0.elapsed_time(e1)
+
+    # ---------------------------------------------------------------- eager timed region: per-launch timer
+    # (every libplora launch bracketed by CUDA events with its algorithmic flops / bytes)
+    timer = ops.KernelTimer()
+    launches0 = ops.launch_count()
+    profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
+    if profile_range:
+        barrier()
+        torch.cuda.profiler.start()
+    ops.set_timer(timer)
+    with ClockSampler(device) as clocks_eager:
+        ms_eager = timed_region(lambda: trainer.step(tokens) if trainer is not None else None, args.steps)
+    ops.set_timer(None)
+    if profile_range:
+        torch.cuda.profiler.stop()
+    launches_eager = ops.launch_count() - launches0
     kstats = timer.summary()
     if os.environ.get("PLORA_RECORDS_OUT") and rank == 0:   # per-launch records for tools/dram_by_shape.py
         Path(os.environ["PLORA_RECORDS_OUT"]).write_text(json.dumps(timer.dump()))
-    ms_max = max_over_ranks(ms)
+    del timer
+    ms_eager_max = max_over_ranks(ms_eager)
     # tokens processed by the whole job: a TP group's ranks share one job's tokens
     tokens_all = sum_over_ranks(float(T) if (tp == 1 or rank % tp == 0) else 0.0)
+
+    # ---------------------------------------------------------------- the step as one CUDA graph
+    graphed = None
+    if trainer is not None and args.graph and not shared:
+        try:
+            graphed = trainer.graphed(tokens, warmup=1)
+        except Exception as exc:   # noqa: BLE001 -- reported in the line; the eager GPU step remains
+            graph_error = f"{type(exc).__name__}: {exc}"[:300]
+            graphed = None
+            torch.cuda.synchronize()
+        else:
+            graph_error = None
+    else:
+        graph_error = "disabled" if not args.graph else ("ranks share a device (gloo)" if shared else None)
+    use_graph = max_over_ranks(0.0 if (graphed is not None or trainer is None) else 1.0) == 0.0 and args.graph \
+        and not shared
+    step_fn = graphed.step if (use_graph and graphed is not None) else (lambda t=None: trainer.step(tokens))
+
+    # ---------------------------------------------------------------- timed region (device): the headline value
+    launches0 = ops.launch_count()
+    with ClockSampler(device) as clocks:
+        ms = timed_region(lambda: step_fn() if trainer is not None else None, args.steps)
+    launches = ops.launch_count() - launches0
+    ms_max = max_over_ranks(ms)
     value = tokens_all * args.steps / (ms_max / 1000.0)
     losses_dev = trainer.losses.clone() if trainer is not None else torch.zeros(0)
 
     # ---------------------------------------------------------------- end-to-end (public API, host buffers)
-    barrier()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
-    e2.record()
     losses_host = torch.zeros(0)
-    for _ in range(args.steps):
+
+    def e2e_step():
+        nonlocal losses_host
         if trainer is not None:
             tokens.copy_(tokens_host, non_blocking=True)
-            losses_host = trainer.step(tokens).cpu()
-    e3.record()
-    barrier()
-    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
+            losses_host = (graphed.step(tokens) if (use_graph and graphed is not None) else trainer.step(tokens)).cpu()
+
+    ms_e2e = max_over_ranks(timed_region(e2e_step, args.steps))
     e2e_value = tokens_all * args.steps / (ms_e2e / 1000.0)
 
     peaks = _peaks()
@@ -495,13 +526,12 @@ def main() -> None:
                                                    "tflops": round(d["flops"] / sec / 1e12, 1)}
             continue
         kernels[kind] = {"launches": d["launches"], "ms_total": round(d["ms"], 3),
-                         "share_of_step": round(d["ms"] / ms, 4) if ms else 0.0}
+                         "share_of_step": round(d["ms"] / ms_eager, 4) if ms_eager else 0.0}
         if d["flops"]:
             kernels[kind]["tflops"] = round(d["flops"] / sec / 1e12, 1)
         if d["bytes"]:
             kernels[kind]["hbm_gbs"] = round(d["bytes"] / sec / 1e9, 1)
             kernels[kind]["hbm_frac"] = round(d["bytes"] / sec / 1e9 / peaks["hbm_gbs"], 3)
-    step_s = ms_max / 1000.0 / args.steps
     useful = useful_flops(cfg, specs, s, tp) if specs else {"base": 0.0, "lora": 0.0, "attention": 0.0}
     useful_all = {k: sum_over_ranks(v) for k, v in useful.items()}   # this rank's share, summed
     per_rank = {"rank": rank, "device": device, "world": dist.get_world_size() if world > 1 else 1,
@@ -539,6 +569,12 @@ def main() -> None:
                 "h2d_bytes_per_step": (tokens_host.numel() * tokens_host.element_size()) if trainer is not None else 0,
                 "d2h_bytes_per_step": losses_host.numel() * losses_host.element_size()},
         "gpu_launches": launches,
+        "step_mode": ("cuda_graph" if use_graph else "eager") + ("" if graph_error is None else
+                                                                 f" (graph not used: {graph_error})"),
+        "eager": {"value": tokens_all * args.steps / (ms_eager_max / 1000.0), "ms_per_step": ms_eager_max / args.steps,
+                  "gpu_launches": launches_eager, "clocks": clocks_eager.summary(),
+                  "note": "eager step with every libplora launch bracketed by CUDA events: the source of "
+                          "roofline, kernels and gemm_shapes"},
         "clocks": clocks.summary(),
         "losses": [round(float(x), 4) for x in losses_dev.tolist()],
         "mem_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),

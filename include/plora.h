@@ -196,8 +196,11 @@ PLORA_API int plora_linear_bwd(void* stream, const plora_pack_t* pack,
  *   chunks: device array [n_chunks][4] int64 =
  *     {master element offset, shadow element offset, n_rows | rpad16 << 32,
  *      adapter | shadow_ld << 32}
- *   hp: device array [n][4] f32 = {lr, weight_decay, unused, unused}
- *   step: optimizer step count (>= 1) used for bias correction. */
+ *   hp: device array [n][4] f32 = {lr, weight_decay, step, unused}
+ *   step: optimizer step count (>= 1) used for bias correction of every adapter, or
+ *     0: each adapter's own count hp[i].z (>= 1, kept on the device by the caller --
+ *     a launch sequence that CUDA graphs can replay, and adapters that joined a
+ *     packed job at different times). */
 PLORA_API int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks,
                 float* param, const float* grad, float* exp_avg, float* exp_avg_sq,
                 void* shadow, const float* hp, float beta1, float beta2, float eps,

@@ -185,11 +185,14 @@ class AdapterBank:
 
     # ------------------------------------------------------------------ optimizer
     def adamw_step(self):
-        """K7: one fused per-adapter AdamW launch over every region of every adapter."""
+        """K7: one fused per-adapter AdamW launch over every region of every adapter.  The
+        step counts live on the device (hp[i].z, incremented here by a device op), so the
+        launch sequence is replayable by a CUDA graph (model.GraphedStep)."""
         from . import ops
 
         self.step_count += 1
-        ops.adamw(self.chunks, self.P, self.G, self.M, self.V, self.shadow, self.hp, self.step_count,
+        self.hp[:, 2] += 1.0
+        ops.adamw(self.chunks, self.P, self.G, self.M, self.V, self.shadow, self.hp, 0,
                   self.betas[0], self.betas[1], self.eps, algo_params=self.trainable_params)
 
     def state_bytes(self) -> int:

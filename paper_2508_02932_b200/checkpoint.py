@@ -66,7 +66,7 @@ def save_adapter(trainer, i: int, directory, config_id: str | None = None, extra
     cfg = {"peft_type": "LORA", "task_type": "CAUSAL_LM", "base_model_name_or_path": trainer.cfg.name,
            "r": spec.rank, "lora_alpha": spec.alpha * spec.rank, "raw_alpha": spec.alpha, "lora_dropout": 0.0,
            "bias": "none", "target_modules": [PEFT_NAMES[t.name].split(".")[-1] for t in trainer.cfg.targets()],
-           "learning_rate": spec.lr, "optimizer_steps": trainer.bank.step_count}
+           "learning_rate": spec.lr, "optimizer_steps": int(trainer.bank.hp[i, 2].item())}
     cfg.update(extra or {})
     (out / "adapter_config.json").write_text(json.dumps(cfg, indent=1))
     return out

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(int64_t n_chunks, const long
                                                     float* __restrict__ exp_avg_sq,
                                                     __nv_bfloat16* __restrict__ shadow,
                                                     const float4* __restrict__ hp, float beta1,
-                                                    float beta2, float eps, float bc1, float bc2_sqrt) {
+                                                    float beta2, float eps, float bc1_all, float bc2_sqrt_all) {
   for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     const longlong4 ch = chunks[c];
     const int64_t p_off = ch.x;
@@ -44,6 +44,11 @@ __global__ void __launch_bounds__(256) adamw_kernel(int64_t n_chunks, const long
     const int32_t sh_ld = static_cast<int32_t>(ch.w >> 32);
     const float4 h = hp[adapter];
     const float lr = h.x, wd = h.y;
+    // bias corrections: one step count for the launch, or the adapter's own (hp.z, on device)
+    // (double, as the host path: 1 - beta2^t cancels catastrophically in fp32 at small t)
+    const float bc1 = bc1_all > 0.f ? bc1_all : static_cast<float>(1.0 - pow(static_cast<double>(beta1), h.z));
+    const float bc2_sqrt = bc1_all > 0.f ? bc2_sqrt_all
+                                         : static_cast<float>(sqrt(1.0 - pow(static_cast<double>(beta2), h.z)));
     const float decay = 1.0f - lr * wd;
     const float step_size = lr / bc1;
     const int32_t n4 = n_rows * rpad / 4;
@@ -90,11 +95,11 @@ extern "C" int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks
                            const float* grad, float* exp_avg, float* exp_avg_sq, void* shadow,
                            const float* hp, float beta1, float beta2, float eps, int64_t step) {
   if (n_chunks <= 0) return 0;
-  if (step < 1) return plora::set_error("adamw: step must be >= 1");
+  if (step < 0) return plora::set_error("adamw: step must be >= 1 (or 0: per-adapter counts in hp[i].z)");
   if (!chunks || !param || !grad || !exp_avg || !exp_avg_sq || !shadow || !hp)
     return plora::set_error("adamw: NULL argument");
-  const double bc1 = 1.0 - pow(static_cast<double>(beta1), static_cast<double>(step));
-  const double bc2 = 1.0 - pow(static_cast<double>(beta2), static_cast<double>(step));
+  const double bc1 = step > 0 ? 1.0 - pow(static_cast<double>(beta1), static_cast<double>(step)) : -1.0;
+  const double bc2 = step > 0 ? 1.0 - pow(static_cast<double>(beta2), static_cast<double>(step)) : 1.0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -702,6 +702,11 @@ class PackedLoraTrainer:
         self.bank.adamw_step()
         return losses
 
+    def graphed(self, tokens: torch.Tensor, warmup: int = 2) -> "GraphedStep":
+        """This trainer's step (forward + backward + AdamW) captured as one CUDA graph
+        (see GraphedStep).  ``warmup`` eager steps run first (they train)."""
+        return GraphedStep(self, tokens, warmup)
+
     # ------------------------------------------------------------------ data
     def synthetic_tokens(self, seed_base: int = 1000, seeds: Sequence[int] | None = None) -> torch.Tensor:
         """tokens ~ U{0..V-1}, seed 1000+i per adapter; ``seeds``
@@ -712,3 +717,45 @@ class PackedLoraTrainer:
             g = torch.Generator(device="cpu").manual_seed(seed_base + i if seeds is None else int(seeds[i]))
             parts.append(torch.randint(0, self.cfg.vocab, (sp.batch * self.s,), generator=g))
         return torch.cat(parts)
+
+
+class GraphedStep:
+    """A packed training step replayed from a CUDA graph.
+
+    Every launch of ``PackedLoraTrainer.step`` -- ~1.3k libplora kernels (tensor maps
+    and LPT schedules baked into their parameters), cuDNN attention, the norms, the CE
+    chunks and the fused AdamW (per-adapter step counts on the device, adapters.py) --
+    is captured once and replayed with one ``cudaGraphLaunch``: no per-kernel host work
+    and no launch gaps.  That is what keeps a small per-GPU share of a planner split
+    (T = 4096 tokens at 8 GPUs, where the eager host enqueue takes as long as the GPU
+    step) device-bound.  Shapes, adapters and the pack are fixed; new tokens are copied
+    into the static input buffer.  Capture uses a private memory pool (the eager step's
+    cached blocks are released first)."""
+
+    def __init__(self, trainer: PackedLoraTrainer, tokens: torch.Tensor, warmup: int = 2):
+        self.trainer = trainer
+        self.tokens = tokens.detach().clone()
+        side = torch.cuda.Stream(device=trainer.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):       # warm-up off the capture stream (allocator, cuDNN plans)
+            for _ in range(warmup):
+                trainer.step(self.tokens)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize(trainer.device)
+        torch.cuda.empty_cache()
+        self.graph = torch.cuda.CUDAGraph()
+        launches0 = ops.launch_count()
+        with torch.cuda.graph(self.graph):
+            self.losses = trainer.step(self.tokens)
+        self.launches_per_step = ops.launch_count() - launches0
+        trainer.bank.step_count -= 1        # the capture enqueued nothing; replays count on the device
+
+    def step(self, tokens: torch.Tensor | None = None) -> torch.Tensor:
+        """One replay (after copying ``tokens`` into the static input); returns the
+        per-adapter losses (device tensor, overwritten by the next replay)."""
+        if tokens is not None:
+            self.tokens.copy_(tokens, non_blocking=True)
+        self.graph.replay()
+        ops.count_launches(self.launches_per_step)
+        self.trainer.bank.step_count += 1
+        return self.losses

@@ -79,6 +79,11 @@ def launch_count() -> int:
     return _LAUNCHES[0]
 
 
+def count_launches(n: int) -> None:
+    """Account for ``n`` libplora kernels launched from a replayed CUDA graph."""
+    _LAUNCHES[0] += n
+
+
 def _lora_work(meta: PackMeta) -> tuple[int, int]:
     """(sum_i T_i r_i, R = sum_i r_i) for the algorithmic-work formulas."""
     if not hasattr(meta, "_work"):

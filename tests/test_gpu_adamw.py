@@ -10,7 +10,10 @@ from paper_2508_02932_b200 import ops
 pytestmark = pytest.mark.gpu
 
 
-def test_adamw_matches_torch():
+@pytest.mark.parametrize("device_steps", [False, True])
+def test_adamw_matches_torch(device_steps):
+    """device_steps: step = 0, each adapter's step count read from hp[i].z on the device
+    (the graph-replayable form; the adapters start at different counts)."""
     torch.manual_seed(0)
     rows, rpads, sh_ld = [37, 64, 5], [16, 32, 64], 64
     lrs, wds = [1e-3, 5e-4, 2e-3], [0.0, 0.01, 0.1]
@@ -35,9 +38,22 @@ def test_adamw_matches_torch():
     hp = torch.tensor([[lr, wd, 0.0, 0.0] for lr, wd in zip(lrs, wds)], device="cuda")
     ref = [torch.nn.Parameter(P[offs[i]:offs[i + 1]].clone()) for i in range(n)]
     opts = [torch.optim.AdamW([ref[i]], lr=lrs[i], weight_decay=wds[i], foreach=False) for i in range(n)]
+    if device_steps:   # adapter i has already taken 2 * i steps (zero gradients: state unchanged but counted)
+        for i in range(n):
+            for _ in range(2 * i):
+                ref[i].grad = torch.zeros_like(ref[i])
+                opts[i].step()
+            M[offs[i]:offs[i + 1]] = opts[i].state[ref[i]]["exp_avg"] if 2 * i else 0.0
+            V[offs[i]:offs[i + 1]] = opts[i].state[ref[i]]["exp_avg_sq"] if 2 * i else 0.0
+            P[offs[i]:offs[i + 1]] = ref[i].detach()
+            hp[i, 2] = float(2 * i)
     for step in range(1, 6):
         G = torch.randn_like(P)
-        ops.adamw(chunks, P, G, M, V, shadow, hp, step)
+        if device_steps:
+            hp[:, 2] += 1.0
+            ops.adamw(chunks, P, G, M, V, shadow, hp, 0)
+        else:
+            ops.adamw(chunks, P, G, M, V, shadow, hp, step)
         for i in range(n):
             ref[i].grad = G[offs[i]:offs[i + 1]].clone()
             opts[i].step()

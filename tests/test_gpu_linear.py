@@ -314,3 +314,44 @@ def test_full_c3_size_packed_linear(d, k):
     y2, _ = ops.linear_fwd(meta2, x, w, True, a_sh, bt_sh)
     base = (x.float() @ w.float().t())
     assert rel(y2.float() - base, 2 * (ry - base)) < 2e-2
+
+
+@pytest.mark.parametrize("d,widths,kmajor", [(4096, [4096, 1024, 1024], True), (4096, [14336, 14336], True),
+                                             (4096, [4096, 1024, 1024], False)])
+def test_grouped_ops_at_c3_widths(d, widths, kmajor):
+    """The grouped pair launches at the C3 widths -- q/k/v (N-segments 4096/1024/1024 and
+    their K-segmented input gradient) and gate/up (K-segments 14336 + 14336) -- take the
+    256 x 512 (NB = 2) tiles: against separate launches and the fp32 reference."""
+    ranks, tokens = [8, 16, 32, 64], [512, 256, 768, 512]
+    meta = build_meta(ranks, tokens, [0.25 * 8, 16.0, 64.0, 256.0]).to("cuda")
+    T, R64, n = meta.total_tokens, meta.rpad64, len(ranks)
+    g = torch.Generator(device="cuda").manual_seed(77)
+    x = torch.randn(T, d, device="cuda", generator=g).to(bf)
+    ws = [((torch.randn(k, d, device="cuda", generator=g) if kmajor else torch.randn(d, k, device="cuda", generator=g))
+           * 0.02).to(bf) for k in widths]
+    bts = [(torch.randn(n, k, R64, device="cuda", generator=g) * 0.02).to(bf) for k in widths]
+    ats = [(torch.randn(n, d, R64, device="cuda", generator=g) * 0.02).to(bf) for _ in widths]
+    hss = [(torch.randn(T, R64, device="cuda", generator=g) * 0.5).to(bf) for _ in widths]
+    for h in hss:
+        for i, r in enumerate(ranks):
+            h[meta.row_offsets[i]:meta.row_offsets[i + 1], r:] = 0
+    if len(widths) == 3:
+        ys = ops.linear_expand_group(meta, x, ws, bts, hss, w_kmajor=kmajor)
+        for w, bt, hs, y in zip(ws, bts, hss, ys):
+            W = w.float().t() if kmajor else w.float()
+            want = x.float() @ W
+            for i, r in enumerate(ranks):
+                s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+                want[s:e] += hs[s:e, :r].float() @ bt[i, :, :r].float().t()
+            assert rel(y, want) < 1e-2
+            assert torch.equal(y, ops.linear_expand(meta, x, w, kmajor, bt, hs))
+    dys = [(torch.randn(T, k, device="cuda", generator=g) * 0.1).to(bf) for k in widths]
+    dx = ops.linear_dx_group(meta, dys, ws, ats, hss, d, w_kmajor=kmajor)
+    want = torch.zeros(T, d, device="cuda")
+    for w, at, dh, dy in zip(ws, ats, hss, dys):
+        W = w.float().t() if kmajor else w.float()          # [d][k]
+        want += dy.float() @ W.t()
+        for i, r in enumerate(ranks):
+            s, e = meta.row_offsets[i], meta.row_offsets[i + 1]
+            want[s:e] += dh[s:e, :r].float() @ at[i, :, :r].float().t()
+    assert rel(dx, want) < 1e-2

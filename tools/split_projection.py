@@ -24,7 +24,7 @@ from paper_2508_02932_b200.sweep.engine import _base  # noqa: E402
 from paper_2508_02932_b200.sweep.jobsplit import split_adapters  # noqa: E402
 
 
-def time_job(cfg_name, idx, steps, warmup):
+def time_job(cfg_name, idx, steps, warmup, kernels=False, graph=False):
     cfg = PRESETS[cfg_name]
     specs, s = bench_adapters(cfg_name)
     sub = [specs[i] for i in idx]
@@ -35,13 +35,28 @@ def time_job(cfg_name, idx, steps, warmup):
         tr.step(tok)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
+    run = tr.graphed(tok, warmup=1).step if graph else (lambda: tr.step(tok))
+    torch.cuda.synchronize()
     e0.record()
+    h0 = time.perf_counter()
     for _ in range(steps):
-        tr.step(tok)
+        run()
+    host_ms = (time.perf_counter() - h0) * 1000 / steps   # host enqueue time (CPU-bound if ~ device time)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     T = tr.T
+    if kernels and not graph:   # one more step with the per-launch timer: per kernel class ms / step
+        from paper_2508_02932_b200 import ops
+        timer = ops.KernelTimer()
+        ops.set_timer(timer)
+        tr.step(tok)
+        ops.set_timer(None)
+        summ = timer.summary()
+        print(json.dumps({"job": list(idx), "T": T, "ms_per_step": round(ms, 2), "host_ms_per_step": round(host_ms, 2),
+                          "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 2)}
+                                      for k, v in summ.items()}}), flush=True)
     del tr
     torch.cuda.empty_cache()
     return T, ms
@@ -53,10 +68,12 @@ def main():
     ap.add_argument("--gpus", default="1,2,4,8")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--kernels", action="store_true", help="print each job's per-kernel-class times")
+    ap.add_argument("--graph", action="store_true", help="time the step replayed from a CUDA graph")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     cache = {}
-    out = {"config": args.config, "projection": []}
+    out = {"config": args.config, "step_mode": "cuda_graph" if args.graph else "eager", "projection": []}
     one = None
     for n in [int(x) for x in args.gpus.split(",")]:
         sp = split_adapters(args.config, n)
@@ -64,7 +81,7 @@ def main():
         for r, idx in enumerate(sp.adapters):
             key = tuple(idx)
             if key not in cache:
-                cache[key] = time_job(args.config, list(idx), args.steps, args.warmup)
+                cache[key] = time_job(args.config, list(idx), args.steps, args.warmup, args.kernels, args.graph)
             T, ms = cache[key]
             ranks.append({"rank": r, "adapters": list(idx), "tokens": T, "ms_per_step": round(ms, 2),
                           "tokens_per_s": round(T / ms * 1000, 1)})
