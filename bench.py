@@ -518,12 +518,16 @@ def main() -> None:
     peaks = _peaks()
     g = kstats.get("gemm", {"ms": 0.0, "flops": 0.0, "launches": 0})
     achieved = g["flops"] / (g["ms"] / 1000.0) / 1e12 if g["ms"] else 0.0
-    kernels, shapes = {}, {}
+    kernels, shapes, lora_shapes = {}, {}, {}
     for kind, d in kstats.items():
         sec = d["ms"] / 1000.0
-        if "[" in kind:   # per-shape GEMM detail
+        if kind.startswith("gemm["):   # per-shape GEMM detail
             shapes[kind[kind.index("[") + 1:-1]] = {"launches": d["launches"], "ms": round(d["ms"], 2),
                                                    "tflops": round(d["flops"] / sec / 1e12, 1)}
+            continue
+        if "[" in kind:                # per-shape LoRA-kernel detail (shrink[K..], segred[M..])
+            lora_shapes[kind] = {"launches": d["launches"], "ms": round(d["ms"], 2),
+                                 "hbm_gbs": round(d["bytes"] / sec / 1e9, 1) if sec else 0.0}
             continue
         kernels[kind] = {"launches": d["launches"], "ms_total": round(d["ms"], 3),
                          "share_of_step": round(d["ms"] / ms_eager, 4) if ms_eager else 0.0}
@@ -565,6 +569,7 @@ def main() -> None:
                                   for k, v in useful_all.items()},
         "kernels": kernels,
         "gemm_shapes": shapes,
+        "lora_shapes": lora_shapes,
         "e2e": {"value": e2e_value, "unit": "tokens/s",
                 "h2d_bytes_per_step": (tokens_host.numel() * tokens_host.element_size()) if trainer is not None else 0,
                 "d2h_bytes_per_step": losses_host.numel() * losses_host.element_size()},

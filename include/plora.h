@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 5
+#define PLORA_ABI_VERSION 6
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -68,10 +68,19 @@ typedef struct plora_pack {
   const int32_t* d_ptiles; /* [n_ptiles][4] = {m0, m_len (1..256), adapter, 0}: CTA-pair tiles */
   const int64_t* h_row_off;/* [n+1] HOST copy of the row offsets (may be NULL): lets the
                               segment reductions balance their tiles across SMs (LPT) */
+  void* d_ws;              /* device workspace of the shrink / segment-reduction kernels
+                              (may be NULL): plora_lora_workspace_bytes() bytes, ZERO-filled
+                              once by the caller; the kernels leave it zeroed.  With it, K2a/K4
+                              and K3/K5 split their long tiles across all SMs (stream-K) --
+                              without it they run whole tiles (fewer SMs busy at small T).
+                              Launches sharing one workspace must be stream-ordered. */
+  int64_t ws_bytes;        /* size of d_ws */
 } plora_pack_t;
 
 /* Library / error plumbing. */
 PLORA_API int plora_abi_version(void);
+/* Bytes of the pack workspace (plora_pack_t.d_ws) on the current device. */
+PLORA_API int64_t plora_lora_workspace_bytes(void);
 PLORA_API const char* plora_last_error(void);
 PLORA_API int plora_device_check(void);   /* 0 iff an sm_100 device is current */
 

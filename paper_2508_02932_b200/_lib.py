@@ -19,6 +19,7 @@ LIB_PATH = Path(os.environ.get("PLORA_LIB", "")).resolve() if os.environ.get("PL
 # Every symbol include/plora.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "plora_abi_version",
+    "plora_lora_workspace_bytes",
     "plora_last_error",
     "plora_device_check",
     "plora_meta_build",
@@ -55,7 +56,7 @@ EXPORTS = (
     "plora_tp_broadcast",
 )
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class PloraError(RuntimeError):
@@ -80,6 +81,8 @@ class PackStruct(ctypes.Structure):
         ("pad_", ctypes.c_int32),
         ("d_ptiles", ctypes.c_void_p),
         ("h_row_off", ctypes.c_void_p),
+        ("d_ws", ctypes.c_void_p),
+        ("ws_bytes", ctypes.c_int64),
     ]
 
 
@@ -95,6 +98,7 @@ _p32 = ctypes.POINTER(ctypes.c_int32)
 
 _SIGNATURES = {
     "plora_abi_version": ([], ctypes.c_int),
+    "plora_lora_workspace_bytes": ([], _i64),
     "plora_last_error": ([], ctypes.c_char_p),
     "plora_device_check": ([], ctypes.c_int),
     "plora_meta_build": ([_i32, _p64, _p64, _p64, _p64, _p32, _p32, _i32, _p32, _p32, _p32, _p32],

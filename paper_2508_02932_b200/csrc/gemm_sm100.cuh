@@ -68,6 +68,12 @@ struct __align__(64) GemmArgs {
   void* out2;
   void* out3;
   const __nv_bfloat16* bias;   // GEMM: optional per-column bias added to the bf16 result
+  // Stream-K partition of SHRINK / SEGRED (sk != 0; see SkIter): fp32 partials of split
+  // tiles in sk_part (2 slots of 128 x BN per CTA), arrival counters in sk_cnt (one per
+  // CTA, zero between launches: the last arriving piece resets its counter).
+  int32_t sk;
+  int32_t* sk_cnt;
+  float* sk_part;
 };
 
 constexpr int kBM = 128;
@@ -136,6 +142,115 @@ struct TileIter {
   __device__ __forceinline__ void next() { j += step; }
 };
 
+// Stream-K partition of the skinny LoRA contractions (K2a/K4 shrink, K3/K5 segment
+// reductions).  Their tiles are few and long (a 128-row shrink tile streams all of h; a
+// segment-reduction tile streams its adapter's whole token segment): at T = 4096 per GPU
+// the shrink has 32 tiles for 148 SMs, at T = 32768 it has 1.8 waves.  Instead of whole
+// tiles, CTA c of G takes the linear k-block range [c W / G, (c+1) W / G) of the tile
+// sequence (W = total k-blocks), so every SM streams the same number of bytes.  A tile cut
+// by CTA boundaries is computed as pieces; every piece stores its fp32 partial in its
+// CTA's slot, and the LAST piece to finish (arrival counter) sums all pieces in piece
+// order -- deterministic for a given pack, no waiting, no atomics on the data.
+//   SHRINK: every tile has ceil(K / 64) k-blocks.  SEGRED: the tiles of adapter a have
+//   max(1, ceil(T_a / 64)) (an empty segment costs one unit and writes zeros).
+struct SkUnit {
+  int tile, kb0, kb1, piece, np, c0;
+  bool first;   // the CTA's first unit (partial slot 0) -- else slot 1
+};
+
+template <int MODE>
+struct SkIter {
+  const GemmArgs& a;
+  int64_t W, x, xend, cstart;
+  int G, c, per, nkb;
+  int ad, len;       // SEGRED: current adapter and its tile length
+  int64_t ap;        // SEGRED: linear start of adapter `ad`'s tiles
+  int64_t tend;
+  SkUnit u;
+
+  __device__ __forceinline__ int seglen(int i) const {
+    const int64_t t = a.row_off[i + 1] - a.row_off[i];
+    return t > 0 ? static_cast<int>((t + kBK - 1) / kBK) : 1;
+  }
+  __device__ __forceinline__ int cta_of(int64_t pos) const { return static_cast<int>(((pos + 1) * G - 1) / W); }
+
+  __device__ __forceinline__ explicit SkIter(const GemmArgs& args) : a(args) {}
+  __device__ __forceinline__ void init() {
+    G = gridDim.x;
+    c = blockIdx.x;
+    per = a.n_ntiles * (MODE == MODE_SEGRED ? a.mt_per : 1);
+    nkb = (a.K + kBK - 1) / kBK;
+    if (MODE == MODE_SEGRED) {
+      W = 0;
+      const int n = a.n_groups / a.mt_per;
+      for (int i = 0; i < n; ++i) W += static_cast<int64_t>(per) * seglen(i);
+      ad = 0;
+      ap = 0;
+      len = n > 0 ? seglen(0) : 1;
+    } else {
+      W = static_cast<int64_t>(a.n_groups) * a.n_ntiles * nkb;
+    }
+    cstart = x = W * c / G;
+    xend = W * (c + 1) / G;
+    if (x < xend) load();
+  }
+  __device__ __forceinline__ void load() {
+    int64_t tstart;
+    if (MODE == MODE_SEGRED) {
+      while (x >= ap + static_cast<int64_t>(per) * len) {
+        ap += static_cast<int64_t>(per) * len;
+        ++ad;
+        len = seglen(ad);
+      }
+      const int j = static_cast<int>((x - ap) / len);
+      u.tile = ad * per + j;
+      tstart = ap + static_cast<int64_t>(j) * len;
+      tend = tstart + len;
+    } else {
+      u.tile = static_cast<int>(x / nkb);
+      tstart = static_cast<int64_t>(u.tile) * nkb;
+      tend = tstart + nkb;
+    }
+    u.kb0 = static_cast<int>(x - tstart);
+    u.kb1 = static_cast<int>((tend < xend ? tend : xend) - tstart);
+    u.c0 = cta_of(tstart);
+    u.np = cta_of(tend - 1) - u.c0 + 1;
+    u.piece = c - u.c0;
+    u.first = x == cstart;
+    pstart0 = W * u.c0 / G == tstart;
+  }
+  bool pstart0;   // piece 0 is its CTA's first unit (partial slot 0)
+  __device__ __forceinline__ bool valid() const { return x < xend; }
+  __device__ __forceinline__ void next() {
+    x = tend < xend ? tend : xend;
+    if (x < xend) load();
+  }
+  // partial slot of piece p of the current unit's tile
+  __device__ __forceinline__ int slot(int p) const { return 2 * (u.c0 + p) + ((p == 0 && !pstart0) ? 1 : 0); }
+};
+
+// The persistent unit loop of the 1-CTA kernel's three warp roles: whole tiles
+// (round-robin or a host LPT list) or stream-K pieces.
+template <int MODE>
+struct UnitLoop {
+  TileIter ti;
+  SkIter<MODE> si;
+  const bool sk;
+  __device__ __forceinline__ UnitLoop(const GemmArgs& a, const SegSched* sched, int total)
+      : ti(sched, total), si(a), sk(MODE != MODE_GEMM && a.sk != 0) {
+    if (sk) si.init();
+  }
+  __device__ __forceinline__ bool valid() const { return sk ? si.valid() : ti.valid(); }
+  __device__ __forceinline__ int tile() const { return sk ? si.u.tile : ti.tile(); }
+  __device__ __forceinline__ int kb0() const { return sk ? si.u.kb0 : 0; }
+  __device__ __forceinline__ int kb1(int nblk) const { return sk ? min(si.u.kb1, nblk) : nblk; }
+  __device__ __forceinline__ bool split() const { return sk && si.u.np > 1; }
+  __device__ __forceinline__ void next() {
+    if (sk) si.next();
+    else    ti.next();
+  }
+};
+
 template <int BN, int MODE>
 __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& a, int idx) {
   TileInfo t;
@@ -182,6 +297,76 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmArgs& a, int idx) {
   t.n0 = nt * BN;
   t.n_main = (t.k_len + kBK - 1) / kBK;
   return t;
+}
+
+// Chunk c (32 fp32 columns) of this thread's TMEM accumulator row.
+__device__ __forceinline__ void tmem_chunk(uint32_t tb, int c, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(tb + c * 32, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Named barrier of the 4 epilogue warps (warps 2..5) of the 1-CTA kernel.
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Stream-K piece of a split tile: store the fp32 partial in this CTA's slot (layout
+// [chunk][quarter][float4 q][lane]: coalesced 512-byte rows), then count the arrival.
+// Returns true on the piece that arrived last -- it owns the fix-up and the output.
+template <int BN, int MODE>
+__device__ __forceinline__ bool sk_arrive(const GemmArgs& a, const SkIter<MODE>& si, uint32_t tb, int quarter,
+                                          int lane, int* flag) {
+  float4* mine = reinterpret_cast<float4*>(a.sk_part) +
+                 static_cast<size_t>(2 * si.c + (si.u.first ? 0 : 1)) * (BN * 32);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_chunk(tb, c, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      __stcg(mine + ((c * 4 + quarter) * 8 + q) * 32 + lane, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+  }
+  __threadfence();
+  epi_bar();
+  if (threadIdx.x == 64) {
+    const int old = atomicAdd(&a.sk_cnt[si.u.c0], 1);
+    const int last = old == si.u.np - 1;
+    if (last) a.sk_cnt[si.u.c0] = 0;   // ready for the next launch (stream-ordered)
+    *reinterpret_cast<volatile int*>(flag) = last;
+  }
+  epi_bar();
+  const bool last = *reinterpret_cast<volatile int*>(flag) != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Chunk c of a split tile: the pieces' partials summed in piece order (this piece's own
+// from TMEM), so the result does not depend on which piece arrived last.
+template <int BN, int MODE>
+__device__ __forceinline__ void sk_gather(const GemmArgs& a, const SkIter<MODE>& si, uint32_t tb, int c, int quarter,
+                                          int lane, float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  for (int p = 0; p < si.u.np; ++p) {
+    if (p == si.u.piece) {
+      float w[32];
+      tmem_chunk(tb, c, w);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += w[j];
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(a.sk_part) + static_cast<size_t>(si.slot(p)) * (BN * 32) +
+                          ((c * 4 + quarter) * 8) * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = __ldcg(src + q * 32);
+        v[4 * q] += f.x;
+        v[4 * q + 1] += f.y;
+        v[4 * q + 2] += f.z;
+        v[4 * q + 3] += f.w;
+      }
+    }
+  }
 }
 
 template <int BN, int MODE, bool B_MN>
@@ -231,10 +416,10 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (TileIter it(sched, total); it.valid(); it.next()) {
+      for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
         const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
-        const int nblk = t.n_main + t.n_lora;
-        for (int b = 0; b < nblk; ++b) {
+        const int b1 = it.kb1(t.n_main + t.n_lora);
+        for (int b = it.kb0(); b < b1; ++b) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = smem + stage * Cfg::kStageBytes;
           uint8_t* sB = sA + Cfg::kABytes;
@@ -280,14 +465,15 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (TileIter it(sched, total); it.valid(); it.next()) {
+    for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
       const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
-      const int nblk = t.n_main + t.n_lora;
-      if (nblk == 0) continue;
+      const int kb_lo = it.kb0();
+      const int kb_hi = it.kb1(t.n_main + t.n_lora);
+      if (kb_hi <= kb_lo) continue;
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int b = 0; b < nblk; ++b) {
+      for (int b = kb_lo; b < kb_hi; ++b) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         uint8_t* sA = smem + stage * Cfg::kStageBytes;
@@ -321,7 +507,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
             else               ad = smem_desc_sw128(a0 + ks * 32, 16, 1024);
             if (!lora && MAIN_B_MN) bd = smem_desc_sw128(b0 + ks * 2048, 8192, 1024);
             else                    bd = smem_desc_sw128(b0 + ks * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, lora ? idesc_lora : idesc_main, (b > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16(d_tmem, ad, bd, lora ? idesc_lora : idesc_main, (b > kb_lo || ks > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
         }
@@ -338,16 +524,17 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (TileIter it(sched, total); it.valid(); it.next()) {
+    int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
       const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
-      const int nblk = t.n_main + t.n_lora;
+      const bool empty = it.kb1(t.n_main + t.n_lora) <= it.kb0();
       if (MODE == MODE_SEGRED) {
         const int ld = args.rpad_off[t.adapter + 1] - args.rpad_off[t.adapter];
         const int64_t goff = static_cast<int64_t>(args.M) * args.rpad_off[t.adapter] +
                              static_cast<int64_t>(t.m0 + row) * ld;
         const bool multi = args.n_multi > 1;
         const bool row_ok = row < t.m_len;
-        if (nblk == 0) {
+        if (empty) {
           if (row_ok) {
             for (int j = 0; j < (multi ? args.n_multi : 1); ++j) {
               float* grow = reinterpret_cast<float*>(j == 0 ? args.out : (j == 1 ? args.out2 : args.out3)) + goff;
@@ -362,25 +549,26 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
         PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+        const bool split = it.split();
+        if (!split || sk_arrive<BN>(args, it.si, tb, quarter, lane, sk_flag)) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tb + c * 32, r);
-          tmem_ld_wait();
-          const int tg = multi ? (c >> 1) : 0;
-          float* grow = reinterpret_cast<float*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) + goff;
-          const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
-          if (row_ok) {
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+            if (split) sk_gather<BN>(args, it.si, tb, c, quarter, lane, v);
+            else       tmem_chunk(tb, c, v);
+            const int tg = multi ? (c >> 1) : 0;
+            float* grow = reinterpret_cast<float*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) + goff;
+            const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
+            if (row_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              if (col0 + j < ld)
-                *reinterpret_cast<float4*>(grow + col0 + j) =
-                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+              for (int j = 0; j < 32; j += 4)
+                if (col0 + j < ld)
+                  *reinterpret_cast<float4*>(grow + col0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
           }
         }
       } else {
-        if (nblk == 0) continue;
+        if (empty) continue;
         PLORA_EPI_WAIT(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -389,55 +577,57 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
         const int64_t orow = static_cast<int64_t>(t.m0 + row) * args.ldo;
         const bool multi = MODE == MODE_SHRINK && args.n_multi > 1;
         const __nv_bfloat16* res = (MODE == MODE_GEMM && args.residual) ? args.residual + orow : nullptr;
+        const bool split = it.split();
+        if (!split || sk_arrive<BN>(args, it.si, tb, quarter, lane, sk_flag)) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tb + c * 32, r);
-          tmem_ld_wait();
-          const int tg = multi ? (c >> 1) : 0;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) +
-                             orow;
-          const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
-          if (row_ok && col0 < args.N) {
+          for (int c = 0; c < BN / 32; ++c) {
             float v[32];
+            if (split) sk_gather<BN>(args, it.si, tb, c, quarter, lane, v);
+            else       tmem_chunk(tb, c, v);
+            const int tg = multi ? (c >> 1) : 0;
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(tg == 0 ? args.out : (tg == 1 ? args.out2 : args.out3)) +
+                               orow;
+            const int col0 = multi ? (c & 1) * 32 : t.n0 + c * 32;
+            if (row_ok && col0 < args.N) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * scale;
-            if (MODE == MODE_GEMM && args.bias != nullptr) {   // round(round(y) + b): as a bf16 bias add
+              for (int j = 0; j < 32; ++j) v[j] *= scale;
+              if (MODE == MODE_GEMM && args.bias != nullptr) {   // round(round(y) + b): as a bf16 bias add
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < args.N)
-                  v[j] = __bfloat162float(__float2bfloat16_rn(v[j])) + __bfloat162float(args.bias[col0 + j]);
-            }
-            if (col0 + 32 <= args.N) {
-              if (res) {
+                for (int j = 0; j < 32; ++j)
+                  if (col0 + j < args.N)
+                    v[j] = __bfloat162float(__float2bfloat16_rn(v[j])) + __bfloat162float(args.bias[col0 + j]);
+              }
+              if (col0 + 32 <= args.N) {
+                if (res) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint4 rv = *reinterpret_cast<const uint4*>(res + col0 + q * 8);
-                  const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                  for (int q = 0; q < 4; ++q) {
+                    const uint4 rv = *reinterpret_cast<const uint4*>(res + col0 + q * 8);
+                    const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
 #pragma unroll
-                  for (int h = 0; h < 4; ++h) {
-                    const float2 f = __bfloat1622float2(rh[h]);
-                    v[q * 8 + 2 * h] += f.x;
-                    v[q * 8 + 2 * h + 1] += f.y;
+                    for (int h = 0; h < 4; ++h) {
+                      const float2 f = __bfloat1622float2(rh[h]);
+                      v[q * 8 + 2 * h] += f.x;
+                      v[q * 8 + 2 * h + 1] += f.y;
+                    }
                   }
                 }
-              }
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint4 w;
-                w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-                w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-                w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-                w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-                *reinterpret_cast<uint4*>(o + col0 + q * 8) = w;
-              }
-            } else {
+                for (int q = 0; q < 4; ++q) {
+                  uint4 w;
+                  w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+                  w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+                  w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+                  w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+                  *reinterpret_cast<uint4*>(o + col0 + q * 8) = w;
+                }
+              } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (col0 + j < args.N) {
-                  float x = v[j];
-                  if (res) x += __bfloat162float(res[col0 + j]);
-                  o[col0 + j] = __float2bfloat16_rn(x);
+                for (int j = 0; j < 32; ++j) {
+                  if (col0 + j < args.N) {
+                    float x = v[j];
+                    if (res) x += __bfloat162float(res[col0 + j]);
+                    o[col0 + j] = __float2bfloat16_rn(x);
+                  }
                 }
               }
             }

@@ -226,7 +226,7 @@ static int launch(const GemmArgs& args, cudaStream_t stream) {
   if (ensure_smem(kern, Cfg::kSmemBytes, configured)) return 1;
   const int total = args.n_groups * args.n_ntiles;
   if (total <= 0) return 0;
-  const int grid = total < num_sms() ? total : num_sms();
+  const int grid = args.sk ? args.sk : (total < num_sms() ? total : num_sms());
   kern<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(args);
   PLORA_CUDA(cudaGetLastError());
   return 0;
@@ -435,6 +435,37 @@ static int run_gemm(cudaStream_t st, const plora_pack_t* pack, int64_t M, int64_
   return w_kmajor ? launch<64, MODE_GEMM, false>(a, st) : launch<64, MODE_GEMM, true>(a, st);
 }
 
+// Stream-K partition of a shrink / segment reduction (SkIter in gemm_sm100.cuh) when the
+// pack carries a workspace: W = total k-blocks (0 = unknown on the host), BN = the
+// launch's accumulator width.  G = min(#SMs, W) CTAs, each with two partial slots.
+static int64_t sk_need_bytes(int G, int BN) { return 1024 + 2LL * G * kBM * BN * 4; }
+
+// At least kSkMinKb k-blocks per CTA: below that the fixed per-CTA cost (prologue,
+// pipeline fill, partial write-back) outweighs the extra SMs.
+static constexpr int64_t kSkMinKb = 8;
+
+static bool setup_sk(GemmArgs& a, const plora_pack_t* pack, int BN, int64_t W) {
+  if (pack->d_ws == nullptr) return false;
+  int G = num_sms();
+  if (W > 0 && W / kSkMinKb < G) G = static_cast<int>(W / kSkMinKb > 0 ? W / kSkMinKb : 1);
+  if (G > 256 || pack->ws_bytes < sk_need_bytes(G, BN)) return false;
+  a.sk = G;
+  a.sk_cnt = static_cast<int32_t*>(pack->d_ws);
+  a.sk_part = reinterpret_cast<float*>(static_cast<char*>(pack->d_ws) + 1024);
+  return true;
+}
+
+// SEGRED stream-K work: per * sum_a max(1, ceil(T_a / 64)) k-blocks (0 without host offsets).
+static int64_t segred_work(const plora_pack_t* pack, int per) {
+  if (pack->h_row_off == nullptr) return 0;
+  int64_t W = 0;
+  for (int i = 0; i < pack->n_adapters; ++i) {
+    const int64_t t = pack->h_row_off[i + 1] - pack->h_row_off[i];
+    W += per * (t > 0 ? (t + kBK - 1) / kBK : 1);
+  }
+  return W;
+}
+
 // Shrink: out[T][64nb] = alpha_i * P[T][K] * L_i[K][64nb]  (L stored [n][K][64nb]).
 static int run_shrink(cudaStream_t st, const plora_pack_t* pack, int64_t K, const void* P,
                       const void* L, void* out) {
@@ -456,6 +487,7 @@ static int run_shrink(cudaStream_t st, const plora_pack_t* pack, int64_t K, cons
   a.K = static_cast<int>(K);
   a.out = out;
   a.ldo = R64;
+  setup_sk(a, pack, 64, static_cast<int64_t>(a.n_groups) * a.n_ntiles * ((K + kBK - 1) / kBK));
   return launch<64, MODE_SHRINK, true>(a, st);
 }
 
@@ -548,7 +580,14 @@ static int run_segred(cudaStream_t st, const plora_pack_t* pack, int64_t Mdim, c
   a.M = static_cast<int>(Mdim);
   a.N = static_cast<int>(R64);
   a.out = G;
-  if (pack->h_row_off != nullptr) {
+  // Stream-K only for a segment reduction too small to fill a quarter of the SMs with whole
+  // tiles (one adapter at T = 4096: 32 tiles); otherwise the LPT schedule, whose CTAs read
+  // the same token rows at the same time (each tile is a 256-byte column stripe of them) --
+  // the stream-K pieces start at staggered rows and lose DRAM locality (same-box A/B at
+  // C3: 47.1 vs 42.6 ms/step, tools/split_projection.py --whole-lora).
+  const bool sk = static_cast<int64_t>(a.n_groups) * a.n_ntiles * 4 <= num_sms() &&
+                  setup_sk(a, pack, 64, segred_work(pack, a.mt_per * a.n_ntiles));
+  if (!sk && pack->h_row_off != nullptr) {
     SegSched sched;
     if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched)) return launch_segred_lpt<64>(a, sched, st);
   }
@@ -581,6 +620,7 @@ static int run_shrink_multi(cudaStream_t st, const plora_pack_t* pack, int64_t K
   a.out3 = n_multi > 2 ? out[2] : nullptr;
   a.ldo = 64;
   a.n_multi = n_multi;
+  setup_sk(a, pack, 64 * n_multi, static_cast<int64_t>(a.n_groups) * ((K + kBK - 1) / kBK));
   return n_multi == 3 ? launch<192, MODE_SHRINK, true>(a, st) : launch<128, MODE_SHRINK, true>(a, st);
 }
 
@@ -609,7 +649,7 @@ static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t M
   a.out2 = n_multi > 1 ? G[1] : nullptr;
   a.out3 = n_multi > 2 ? G[2] : nullptr;
   a.n_multi = n_multi;
-  if (pack->h_row_off != nullptr) {
+  if (pack->h_row_off != nullptr) {   // whole tiles (LPT): see run_segred
     SegSched sched;
     if (segred_schedule(pack, a.mt_per, a.n_ntiles, &sched))
       return n_multi == 3 ? launch_segred_lpt<192>(a, sched, st) : launch_segred_lpt<128>(a, sched, st);
@@ -624,6 +664,8 @@ using namespace plora;
 extern "C" {
 
 int plora_abi_version(void) { return PLORA_ABI_VERSION; }
+
+int64_t plora_lora_workspace_bytes(void) { return sk_need_bytes(num_sms(), 192); }
 
 const char* plora_last_error(void) { return g_last_error.c_str(); }
 

@@ -49,7 +49,7 @@ class KernelTimer:
         out: dict = {}
         for kind, e0, e1, fl, nb, detail, _ in self.records:
             ms = e0.elapsed_time(e1)
-            keys = [kind] + ([f"{kind}[{detail}]"] if detail is not None and kind == "gemm" else [])
+            keys = [kind] + ([f"{kind}[{detail}]"] if detail is not None else [])
             for key in keys:
                 d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
                 d["launches"] += 1
@@ -82,6 +82,32 @@ def launch_count() -> int:
 def count_launches(n: int) -> None:
     """Account for ``n`` libplora kernels launched from a replayed CUDA graph."""
     _LAUNCHES[0] += n
+
+
+_WS: dict = {}
+
+
+def _workspace() -> torch.Tensor:
+    """The pack workspace of the stream-K shrink / segment-reduction kernels for the
+    current (device, stream): zero-filled once, left zeroed by the kernels, so launches
+    on one stream share it (include/plora.h, plora_pack_t.d_ws).  Created under CUDA-graph
+    capture it comes from the graph's pool and its zero-fill is part of the graph."""
+    dev = torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream().cuda_stream)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = torch.zeros(int(_lib.lib().plora_lora_workspace_bytes()), dtype=torch.uint8, device=f"cuda:{dev}")
+        _WS[key] = ws
+    return ws
+
+
+def _pack(meta: PackMeta):
+    """meta's plora_pack_t with the current stream's workspace attached."""
+    s = meta.struct
+    ws = _workspace()
+    s.d_ws = ws.data_ptr()
+    s.ws_bytes = ws.numel()
+    return s
 
 
 def _lora_work(meta: PackMeta) -> tuple[int, int]:
@@ -162,7 +188,7 @@ def linear_fwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
     _on_current_device(x, "x")
     _lora_shapes(meta, d, a_sh, hs_out, T)
     _size(bt_sh, "bt_sh", meta.n_adapters * k * meta.rpad64)
-    s = meta.struct
+    s = _pack(meta)
     if _TIMER is not None:
         shrink(meta, x, a_sh, hs_out)
         linear_expand(meta, x, w, w_kmajor, bt_sh, hs_out, y_out, residual)
@@ -181,7 +207,7 @@ def shrink(meta: PackMeta, p: torch.Tensor, l_sh: torch.Tensor, out: torch.Tenso
     _on_current_device(p, "p")
     _lora_shapes(meta, K, l_sh, out, meta.total_tokens)
     t = _TIMER.start() if _TIMER else None
-    _lib.check(_lib.lib().plora_lora_shrink(_stream(), ctypes.byref(meta.struct), K, _need(p, "p"),
+    _lib.check(_lib.lib().plora_lora_shrink(_stream(), ctypes.byref(_pack(meta)), K, _need(p, "p"),
                                             _need(l_sh, "l_sh"), _need(out, "out")), "plora_lora_shrink")
     _LAUNCHES[0] += 1
     if t is not None:
@@ -197,7 +223,7 @@ def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) ->
     _size(q, "q", meta.total_tokens * meta.rpad64)
     _size(g, "g", Mdim * meta.rpad16_total)
     t = _TIMER.start() if _TIMER else None
-    _lib.check(_lib.lib().plora_lora_segred(_stream(), ctypes.byref(meta.struct), Mdim, _need(p, "p"),
+    _lib.check(_lib.lib().plora_lora_segred(_stream(), ctypes.byref(_pack(meta)), Mdim, _need(p, "p"),
                                             _need(q, "q"), _need(g, "g", torch.float32)), "plora_lora_segred")
     _LAUNCHES[0] += 1
     if t is not None:
@@ -222,7 +248,7 @@ def shrink_multi(meta: PackMeta, p: torch.Tensor, l_shs, outs) -> list:
     t = _TIMER.start() if _TIMER else None
     lp, _k1 = _ptr_array(l_shs, "l_sh")
     op, _k2 = _ptr_array(outs, "out")
-    _lib.check(_lib.lib().plora_lora_shrink_multi(_stream(), ctypes.byref(meta.struct), K, _need(p, "p"),
+    _lib.check(_lib.lib().plora_lora_shrink_multi(_stream(), ctypes.byref(_pack(meta)), K, _need(p, "p"),
                                                   len(outs), lp, op), "plora_lora_shrink_multi")
     _LAUNCHES[0] += 1 if meta.nb == 1 else len(outs)
     if t is not None:
@@ -243,7 +269,7 @@ def segred_multi(meta: PackMeta, p: torch.Tensor, qs, gs) -> list:
     t = _TIMER.start() if _TIMER else None
     qp, _k1 = _ptr_array(qs, "q")
     gp, _k2 = _ptr_array(gs, "g", torch.float32)
-    _lib.check(_lib.lib().plora_lora_segred_multi(_stream(), ctypes.byref(meta.struct), Mdim, _need(p, "p"),
+    _lib.check(_lib.lib().plora_lora_segred_multi(_stream(), ctypes.byref(_pack(meta)), Mdim, _need(p, "p"),
                                                   len(gs), qp, gp), "plora_lora_segred_multi")
     _LAUNCHES[0] += 1 if meta.nb == 1 else len(gs)
     if t is not None:
@@ -278,7 +304,7 @@ def linear_expand_group(meta: PackMeta, x: torch.Tensor, ws, bt_shs, hss, w_kmaj
         bip = ctypes.cast(barr, ctypes.POINTER(ctypes.c_void_p))
     else:
         bip = None
-    _lib.check(_lib.lib().plora_linear_expand_group(_stream(), ctypes.byref(meta.struct), _need(x, "x"), d, len(ws),
+    _lib.check(_lib.lib().plora_linear_expand_group(_stream(), ctypes.byref(_pack(meta)), _need(x, "x"), d, len(ws),
                                                     karr, wp, int(w_kmajor), bp, hp, yp, bip),
                "plora_linear_expand_group")
     _LAUNCHES[0] += 1
@@ -310,7 +336,7 @@ def linear_gate_up_swiglu(meta: PackMeta, x: torch.Tensor, w_gate: torch.Tensor,
         act = torch.empty_like(g)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_linear_gate_up_swiglu(
-        _stream(), ctypes.byref(meta.struct), _need(x, "x"), d, ffn, _need(w_gate, "w_gate"), _need(w_up, "w_up"),
+        _stream(), ctypes.byref(_pack(meta)), _need(x, "x"), d, ffn, _need(w_gate, "w_gate"), _need(w_up, "w_up"),
         _need(bt_gate, "bt_gate"), _need(bt_up, "bt_up"), _need(hs_gate, "hs_gate"), _need(hs_up, "hs_up"),
         _need(g, "g"), _need(u, "u"), _need(act, "act")), "plora_linear_gate_up_swiglu")
     _LAUNCHES[0] += 1
@@ -339,7 +365,7 @@ def linear_dx_group(meta: PackMeta, dys, ws, a_shs, dhs, d: int, w_kmajor: bool 
     wp, _k2 = _ptr_array(ws, "w")
     ap, _k3 = _ptr_array(a_shs, "a_sh")
     hp, _k4 = _ptr_array(dhs, "dh")
-    _lib.check(_lib.lib().plora_linear_dx_group(_stream(), ctypes.byref(meta.struct), len(dys), yp, karr, wp,
+    _lib.check(_lib.lib().plora_linear_dx_group(_stream(), ctypes.byref(_pack(meta)), len(dys), yp, karr, wp,
                                                 int(w_kmajor), ap, hp, d, _need(dx_out, "dx"), dx_out.stride(0),
                                                 _need(dx_residual, "dx_residual", allow_none=True)),
                "plora_linear_dx_group")
@@ -363,7 +389,7 @@ def linear_expand(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bo
     _on_current_device(x, "x")
     _size(bt_sh, "bt_sh", meta.n_adapters * k * meta.rpad64)
     _size(hs, "hs", T * meta.rpad64)
-    s = meta.struct
+    s = _pack(meta)
     t = _TIMER.start() if _TIMER else None
     _lib.check(_lib.lib().plora_linear_expand(
         _stream(), ctypes.byref(s), _need(x, "x"), d, k, _need(w, "w"), int(w_kmajor),
@@ -399,7 +425,7 @@ def linear_bwd(meta: PackMeta, x: torch.Tensor, w: torch.Tensor, w_kmajor: bool,
     _size(dy, "dy", T * k)
     _size(grad_a, "grad_a", d * meta.rpad16_total)
     _size(grad_b, "grad_b", k * meta.rpad16_total)
-    s = meta.struct
+    s = _pack(meta)
     if _TIMER is not None:
         shrink(meta, dy, bt_sh, dh_ws)                       # Case 2 (K4)
         if grad_b is not None:

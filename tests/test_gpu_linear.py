@@ -106,8 +106,22 @@ def test_unaligned_segments_pair_tiles(kmajor):
         assert rel(blk_b[:, :r], rdB[i]) < 5e-3, ("dB", i)
 
 
-def test_packing_invariance():
-    """Adapter i's outputs/grads in a pack equal running it alone."""
+def _whole_tiles(meta):
+    """plora_pack_t without a workspace: the LoRA kernels run whole tiles (no stream-K)."""
+    s = meta.struct
+    s.d_ws = None
+    s.ws_bytes = 0
+    return s
+
+
+@pytest.mark.parametrize("stream_k", [False, True])
+def test_packing_invariance(stream_k, monkeypatch):
+    """Adapter i's outputs/grads in a pack equal running it alone.  With
+    whole tiles bit for bit; with the stream-K LoRA kernels the split points of a tile
+    depend on the rest of the pack, so the fp32 partial sums associate differently:
+    equal to fp32 rounding (bf16 outputs within a last-bit flip)."""
+    if not stream_k:
+        monkeypatch.setattr(ops, "_pack", _whole_tiles)
     d, k = 1024, 2048
     ranks, tokens = [8, 64, 16], [256, 384, 128]
     meta, x, w, a_sh, bt_sh, dy = make(ranks, tokens, d, k, seed=5)
@@ -124,12 +138,14 @@ def test_packing_invariance():
         gbs = torch.empty(k * solo.rpad16_total, device="cuda")
         dxs = ops.linear_bwd(solo, x[s:e].contiguous(), w, True, a_sh[i:i + 1].contiguous(),
                              bt_sh[i:i + 1].contiguous(), hss, dy[s:e].contiguous(), gas, gbs)
-        assert torch.equal(ys, y[s:e])          # same tiles, same math: bit-identical
-        assert torch.equal(dxs, dx[s:e])
         off = int(meta.rpad_off[i])
         rp = solo.rpad16_total
-        assert torch.equal(gas, ga[d * off: d * (off + rp)])
-        assert torch.equal(gbs, gb[k * off: k * (off + rp)])
+        pairs = ((ys, y[s:e]), (dxs, dx[s:e]), (gas, ga[d * off: d * (off + rp)]), (gbs, gb[k * off: k * (off + rp)]))
+        for got, want in pairs:
+            if stream_k:
+                assert rel(got, want) < 2e-3
+            else:
+                assert torch.equal(got, want)   # same tiles, same math: bit-identical
 
 
 def test_deterministic_grads():

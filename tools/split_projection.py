@@ -70,7 +70,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--kernels", action="store_true", help="print each job's per-kernel-class times")
     ap.add_argument("--graph", action="store_true", help="time the step replayed from a CUDA graph")
+    ap.add_argument("--whole-lora", action="store_true",
+                    help="A/B: LoRA kernels without the pack workspace (whole tiles, no stream-K)")
     args = ap.parse_args()
+    if args.whole_lora:
+        from paper_2508_02932_b200 import ops
+
+        def whole(meta):
+            s = meta.struct
+            s.d_ws = None
+            s.ws_bytes = 0
+            return s
+        ops._pack = whole
     torch.cuda.set_device(0)
     cache = {}
     out = {"config": args.config, "step_mode": "cuda_graph" if args.graph else "eager", "projection": []}
