@@ -454,11 +454,13 @@ def main() -> None:
         barrier()
         return e0.elapsed_time(e1)
 
-    # ---------------------------------------------------------------- eager timed region: per-launch timer
-    # (every libplora launch bracketed by CUDA events with its algorithmic flops / bytes)
-    timer = ops.KernelTimer()
+    # ---------------------------------------------------------------- eager timed region (plain eager step)
+    # With PLORA_PROFILE_RANGE=1 (ncu --profile-from-start off) this region is the profiled one and
+    # its libplora launches carry the per-launch timer (PLORA_RECORDS_OUT: records for
+    # tools/dram_by_shape.py, matched launch by launch with ncu's list).
+    profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"
+    timer = ops.KernelTimer() if profile_range else None
     launches0 = ops.launch_count()
-    profile_range = os.environ.get("PLORA_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
     if profile_range:
         barrier()
         torch.cuda.profiler.start()
@@ -469,14 +471,54 @@ def main() -> None:
     if profile_range:
         torch.cuda.profiler.stop()
     launches_eager = ops.launch_count() - launches0
-    kstats = timer.summary()
-    if os.environ.get("PLORA_RECORDS_OUT") and rank == 0:   # per-launch records for tools/dram_by_shape.py
+    if timer is not None and os.environ.get("PLORA_RECORDS_OUT") and rank == 0:
         Path(os.environ["PLORA_RECORDS_OUT"]).write_text(json.dumps(timer.dump()))
-    del timer
     ms_eager_max = max_over_ranks(ms_eager)
     # tokens processed by the whole job: a TP group's ranks share one job's tokens
     tokens_all = sum_over_ranks(float(T) if (tp == 1 or rank % tp == 0) else 0.0)
 
+    # ---------------------------------------------------------------- per-launch kernel stats
+    # The step captured as a CUDA graph with every libplora launch bracketed by event-record
+    # nodes (KernelTimer(external=True)) and replayed: per-launch device times with no host
+    # enqueue gaps (the eager step's host work per launch is as long as a small LoRA kernel,
+    # so eager per-launch events time the host).  Source of roofline, kernels, gemm_shapes.
+    kstats, kstats_mode = None, None
+    if trainer is not None and args.graph and not shared:
+        try:
+            kt = ops.KernelTimer(external=True)
+            ops.set_timer(kt)
+            try:
+                tg = trainer.graphed(tokens, warmup=0)
+            finally:
+                ops.set_timer(None)
+            tg.step()                          # warm replay
+            torch.cuda.synchronize()
+            kstats = {}
+            for _ in range(max(1, min(args.steps, 3))):
+                tg.step()
+                for key, d in kt.summary().items():
+                    acc = kstats.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+                    for f in acc:
+                        acc[f] += d[f]
+            kstats_steps = max(1, min(args.steps, 3))
+            kstats_mode = f"cuda graph with event-record nodes around every libplora launch, {kstats_steps} replays"
+            del tg, kt
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+        except Exception as exc:   # noqa: BLE001 -- fall back to the eager per-launch timer
+            kstats, kstats_mode = None, f"graph timer failed ({type(exc).__name__}: {str(exc)[:120]}); eager"
+            ops.set_timer(None)
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    if kstats is None:
+        kt = ops.KernelTimer()
+        ops.set_timer(kt)
+        timed_region(lambda: trainer.step(tokens) if trainer is not None else None, args.steps)
+        ops.set_timer(None)
+        kstats = kt.summary()
+        kstats_steps = args.steps
+        kstats_mode = (kstats_mode or "") + "eager step with every libplora launch bracketed by CUDA events"
+        del kt
     # ---------------------------------------------------------------- the step as one CUDA graph
     graphed = None
     if trainer is not None and args.graph and not shared:
@@ -530,7 +572,7 @@ def main() -> None:
                                  "hbm_gbs": round(d["bytes"] / sec / 1e9, 1) if sec else 0.0}
             continue
         kernels[kind] = {"launches": d["launches"], "ms_total": round(d["ms"], 3),
-                         "share_of_step": round(d["ms"] / ms_eager, 4) if ms_eager else 0.0}
+                         "share_of_step": round(d["ms"] / kstats_steps / (ms / args.steps), 4) if ms else 0.0}
         if d["flops"]:
             kernels[kind]["tflops"] = round(d["flops"] / sec / 1e12, 1)
         if d["bytes"]:
@@ -577,9 +619,9 @@ def main() -> None:
         "step_mode": ("cuda_graph" if use_graph else "eager") + ("" if graph_error is None else
                                                                  f" (graph not used: {graph_error})"),
         "eager": {"value": tokens_all * args.steps / (ms_eager_max / 1000.0), "ms_per_step": ms_eager_max / args.steps,
-                  "gpu_launches": launches_eager, "clocks": clocks_eager.summary(),
-                  "note": "eager step with every libplora launch bracketed by CUDA events: the source of "
-                          "roofline, kernels and gemm_shapes"},
+                  "gpu_launches": launches_eager, "clocks": clocks_eager.summary()},
+        "kernel_stats": {"mode": kstats_mode, "steps": kstats_steps,
+                         "note": "source of roofline, kernels, gemm_shapes and lora_shapes"},
         "clocks": clocks.summary(),
         "losses": [round(float(x), 4) for x in losses_dev.tolist()],
         "mem_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),

@@ -231,13 +231,16 @@ struct SkIter {
 
 // The persistent unit loop of the 1-CTA kernel's three warp roles: whole tiles
 // (round-robin or a host LPT list) or stream-K pieces.
-template <int MODE>
+// SK is a compile-time choice (the launcher instantiates the stream-K kernel only when the
+// pack carries a workspace and the launch is short of SMs), so whole-tile launches run
+// without the stream-K bookkeeping in their registers.
+template <int MODE, bool SK>
 struct UnitLoop {
   TileIter ti;
   SkIter<MODE> si;
-  const bool sk;
+  static constexpr bool sk = SK && MODE != MODE_GEMM;
   __device__ __forceinline__ UnitLoop(const GemmArgs& a, const SegSched* sched, int total)
-      : ti(sched, total), si(a), sk(MODE != MODE_GEMM && a.sk != 0) {
+      : ti(sched, total), si(a) {
     if (sk) si.init();
   }
   __device__ __forceinline__ bool valid() const { return sk ? si.valid() : ti.valid(); }
@@ -369,7 +372,7 @@ __device__ __forceinline__ void sk_gather(const GemmArgs& a, const SkIter<MODE>&
   }
 }
 
-template <int BN, int MODE, bool B_MN>
+template <int BN, int MODE, bool B_MN, bool SK>
 __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* sched) {
   using Cfg = GemmCfg<BN>;
   constexpr bool A_MN = (MODE == MODE_SEGRED);
@@ -416,7 +419,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
+      for (UnitLoop<MODE, SK> it(args, sched, total); it.valid(); it.next()) {
         const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
         const int b1 = it.kb1(t.n_main + t.n_lora);
         for (int b = it.kb0(); b < b1; ++b) {
@@ -465,7 +468,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
+    for (UnitLoop<MODE, SK> it(args, sched, total); it.valid(); it.next()) {
       const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
       const int kb_lo = it.kb0();
       const int kb_hi = it.kb1(t.n_main + t.n_lora);
@@ -525,7 +528,7 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
     int acc = 0;
     uint32_t acc_phase = 0;
     int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
-    for (UnitLoop<MODE> it(args, sched, total); it.valid(); it.next()) {
+    for (UnitLoop<MODE, SK> it(args, sched, total); it.valid(); it.next()) {
       const TileInfo t = decode_tile<BN, MODE>(args, it.tile());
       const bool empty = it.kb1(t.n_main + t.n_lora) <= it.kb0();
       if (MODE == MODE_SEGRED) {
@@ -649,16 +652,16 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
   }
 }
 
-template <int BN, int MODE, bool B_MN>
+template <int BN, int MODE, bool B_MN, bool SK = false>
 __global__ void __launch_bounds__(kThreads, 1) plora_gemm_kernel(const __grid_constant__ GemmArgs args) {
-  gemm_body<BN, MODE, B_MN>(args, nullptr);
+  gemm_body<BN, MODE, B_MN, SK>(args, nullptr);
 }
 
 // Segment reduction with a host-computed LPT tile schedule (see SegSched).
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __grid_constant__ GemmArgs args,
                                                                         const __grid_constant__ SegSched sched) {
-  gemm_body<BN, MODE_SEGRED, true>(args, &sched);
+  gemm_body<BN, MODE_SEGRED, true, false>(args, &sched);
 }
 
 // ============================================================================
@@ -681,6 +684,12 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 #endif
 #ifndef PLORA_PAIR_BUFS
 #define PLORA_PAIR_BUFS 4     // NB = 2 epilogue staging buffers per warp
+#endif
+#ifndef PLORA_STORE_EVICT_FIRST
+#define PLORA_STORE_EVICT_FIRST 0   // pair-epilogue TMA stores with an L2 evict_first policy (experiment knob)
+#endif
+#ifndef PLORA_SWIGLU_DIRECT
+#define PLORA_SWIGLU_DIRECT 2       // SwiGLU epilogue: gate/up chunk pairs stored before the accumulator release
 #endif
 #ifndef PLORA_PAIR_KDIRECT
 #define PLORA_PAIR_KDIRECT 4  // NB = 2 chunks stored before the accumulator release (rest parked)
@@ -851,7 +860,11 @@ __device__ __forceinline__ void pair_emit_chunk(const PairOut& po, uint8_t* stg,
     __syncwarp();
     if (lane == 0) {
       if (po.accumulate) tma_reduce_add_2d(po.tm, buf, col0, m0);
+#if PLORA_STORE_EVICT_FIRST
+      else               tma_store_2d_hint(po.tm, buf, col0, m0, l2_policy_evict_first());
+#else
       else               tma_store_2d(po.tm, buf, col0, m0);
+#endif
       bulk_commit();
     }
     ++issued;
@@ -1069,7 +1082,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
     if constexpr (EPI == EPI_SWIGLU) {
       // paired gate/up tile: warp (quarter, chalf) owns gate chunks chalf*4+i (TMEM cols
       // 0..255) and the matching up chunks 8+chalf*4+i; per pair it stores g, u and act.
-      constexpr int kPairs = 4, kDirectPairs = 2;
+      constexpr int kPairs = 4, kDirectPairs = PLORA_SWIGLU_DIRECT;
       for (int idx = cluster; idx < total; idx += n_clusters) {
         const PairTile t = decode_pair_tile<NB>(p, idx);
         const int m0 = t.m0 + static_cast<int>(rank) * 128 + quarter * 32;

@@ -218,18 +218,27 @@ static int num_sms() {
   return cached[dev];
 }
 
-template <int BN, int MODE, bool B_MN>
-static int launch(const GemmArgs& args, cudaStream_t stream) {
+template <int BN, int MODE, bool B_MN, bool SK>
+static int launch_as(const GemmArgs& args, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  auto kern = plora_gemm_kernel<BN, MODE, B_MN>;
+  auto kern = plora_gemm_kernel<BN, MODE, B_MN, SK>;
   static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
   if (ensure_smem(kern, Cfg::kSmemBytes, configured)) return 1;
   const int total = args.n_groups * args.n_ntiles;
   if (total <= 0) return 0;
-  const int grid = args.sk ? args.sk : (total < num_sms() ? total : num_sms());
+  const int grid = SK ? args.sk : (total < num_sms() ? total : num_sms());
   kern<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(args);
   PLORA_CUDA(cudaGetLastError());
   return 0;
+}
+
+// The stream-K instantiation exists for the skinny LoRA modes only (setup_sk sets args.sk).
+template <int BN, int MODE, bool B_MN>
+static int launch(const GemmArgs& args, cudaStream_t stream) {
+  if constexpr (MODE != MODE_GEMM) {
+    if (args.sk) return launch_as<BN, MODE, B_MN, true>(args, stream);
+  }
+  return launch_as<BN, MODE, B_MN, false>(args, stream);
 }
 
 static int pick_bn(int64_t N) { return N >= 256 ? 256 : (N > 64 ? 128 : 64); }
@@ -444,8 +453,18 @@ static int64_t sk_need_bytes(int G, int BN) { return 1024 + 2LL * G * kBM * BN *
 // pipeline fill, partial write-back) outweighs the extra SMs.
 static constexpr int64_t kSkMinKb = 8;
 
+#ifndef PLORA_SK_MAX_WAVES
+#define PLORA_SK_MAX_WAVES 1   // stream-K below this many whole-tile waves (build-time knob)
+#endif
+
 static bool setup_sk(GemmArgs& a, const plora_pack_t* pack, int BN, int64_t W) {
-  if (pack->d_ws == nullptr) return false;
+  // Whole tiles when they fill every SM at least once: at C3 (T = 32768, 1.7 waves) the
+  // stream-K split times the same in isolation and lost 1.3% of the step in a same-box
+  // A/B (profiles/r2_streamk_gate_ab.log); below one wave (planner-split ranks, T <= 16384)
+  // it is 1.4-2.4x faster (profiles/r2_split_kernels_streamk.log).
+  if (pack->d_ws == nullptr ||
+      a.n_groups * static_cast<int64_t>(a.n_ntiles) >= static_cast<int64_t>(PLORA_SK_MAX_WAVES) * num_sms())
+    return false;
   int G = num_sms();
   if (W > 0 && W / kSkMinKb < G) G = static_cast<int>(W / kSkMinKb > 0 ? W / kSkMinKb : 1);
   if (G > 256 || pack->ws_bytes < sk_need_bytes(G, BN)) return false;

@@ -29,17 +29,21 @@ class KernelTimer:
     (``nbytes``: the roofline bytes of the HBM-bound kernels; ``algo_bytes``: operand +
     output bytes of every launch, the denominator of ncu's DRAM-traffic ratio)."""
 
-    def __init__(self):
+    def __init__(self, external: bool = False):
+        # external=True: the events become event-record nodes when the timed step is captured
+        # into a CUDA graph, so every replay re-times each launch on the device without the
+        # eager step's host enqueue gaps (bench.py's kernel-stats pass)
         self.records: list = []
+        self.external = external
 
     def start(self):
-        e = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True, external=self.external)
         e.record()
         return e
 
     def stop(self, kind: str, e0, flops: float = 0.0, nbytes: float = 0.0, detail: str | None = None,
              algo_bytes: float | None = None):
-        e1 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=self.external)
         e1.record()
         self.records.append((kind, e0, e1, flops, nbytes, detail, nbytes if algo_bytes is None else algo_bytes))
 

@@ -27,18 +27,22 @@ def whole(meta):
 
 
 def timeit(fn, reps=20, warm=3):
+    """Median device time of fn: all reps are enqueued behind a 50 ms sleep kernel, so the
+    events time the kernel back to back (no host launch latency inside the bracket)."""
     for _ in range(warm):
         fn()
-    ts = []
+    torch.cuda.synchronize()
+    torch.cuda._sleep(int(50e-3 * 1.9e9))
+    evs = []
     for _ in range(reps):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
         e.record()
-        torch.cuda.synchronize()
-        ts.append(s.elapsed_time(e))
-    ts.sort()
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    ts = sorted(s.elapsed_time(e) for s, e in evs)
     return ts[len(ts) // 2]
 
 
