@@ -30,6 +30,8 @@ EXPORTS = (
     "plora_lora_segred",
     "plora_lora_shrink_multi",
     "plora_lora_segred_multi",
+    "plora_lora_dual_workspace_bytes",
+    "plora_lora_dual",
     "plora_linear_expand",
     "plora_linear_expand_group",
     "plora_add_row_bias",
@@ -56,7 +58,7 @@ EXPORTS = (
     "plora_tp_broadcast",
 )
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 class PloraError(RuntimeError):
@@ -113,6 +115,9 @@ _SIGNATURES = {
                                  ctypes.POINTER(_vp)], ctypes.c_int),
     "plora_lora_segred_multi": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _i32, ctypes.POINTER(_vp),
                                  ctypes.POINTER(_vp)], ctypes.c_int),
+    "plora_lora_dual_workspace_bytes": ([ctypes.POINTER(PackStruct), _i64, _p32], _i64),
+    "plora_lora_dual": ([_vp, ctypes.POINTER(PackStruct), _i64, _p32, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
+                        ctypes.c_int),
     "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                              _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_expand_group": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i32, _p64, ctypes.POINTER(_vp),

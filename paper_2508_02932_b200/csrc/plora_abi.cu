@@ -21,6 +21,7 @@
 
 #include "../../include/plora.h"
 #include "gemm_sm100.cuh"
+#include "dual_sm100.cuh"
 
 namespace plora {
 
@@ -680,6 +681,102 @@ static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t M
 
 using namespace plora;
 
+// ---------------------------------------------------------------- fused K3 + K4 (dual_sm100.cuh)
+// Plan of the one-dY-pass kernel for (pack, k): units of up to kDualRC 128-row m-tiles of
+// one adapter x nc column chunks.  nc grows (1, 2, 4) until the units cover 3/4 of the SMs;
+// a pack with fewer than half the SMs' worth of units (planner-split ranks at small T) or
+// with rank blocks > 1 / k not a multiple of 128 is not eligible (separate stream-K
+// kernels instead).  Returns the workspace bytes (partials) or -1 when not eligible.
+struct DualPlan {
+  DualSched sched;
+  DualFix fix;
+  int64_t part_b_floats;
+  int64_t part_h_floats;
+};
+
+static int64_t dual_plan(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, DualPlan* plan) {
+  const int n = pack->n_adapters;
+  if (!pack->h_row_off || !h_rpad_off || pack->nb != 1 || k <= 0 || k % 128 || n > kDualMaxAdapters ||
+      k > (1 << 24))
+    return -1;
+  int64_t chunks = 0;
+  for (int a = 0; a < n; ++a) {
+    const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
+    chunks += (tiles + kDualRC - 1) / kDualRC;
+  }
+  const int sms = num_sms();
+  int nc = 1;
+  while (chunks * nc < sms * 3 / 4 && nc < 4 && k / 128 >= 2 * nc) nc *= 2;
+  if (chunks == 0 || chunks * nc < sms / 2 || chunks * nc > kDualMaxUnits) return -1;
+  const int kc = static_cast<int>(((k + nc - 1) / nc + 127) / 128 * 128);
+  nc = static_cast<int>((k + kc - 1) / kc);
+  DualSched& sc = plan->sched;
+  DualFix& f = plan->fix;
+  sc.nc = f.nc = nc;
+  sc.kc = f.kc = kc;
+  sc.k = f.k = static_cast<int>(k);
+  f.n = n;
+  int u = 0;
+  int64_t g = 0, boff = 0;   // boff in floats
+  for (int a = 0; a < n; ++a) {
+    f.ubase[a] = u;
+    const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
+    const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
+    if (rp <= 0 || rp > 64) return -1;
+    for (int64_t q = 0; q < tiles; q += kDualRC) {
+      const int rc = static_cast<int>(tiles - q < kDualRC ? tiles - q : kDualRC);
+      if (g + q >= (1 << 20)) return -1;
+      for (int c = 0; c < nc; ++c) {
+        sc.unit[u] = static_cast<uint32_t>(g + q) | static_cast<uint32_t>(rc - 1) << 20 | static_cast<uint32_t>(c) << 22;
+        sc.boff[u] = static_cast<uint32_t>(boff / 16);
+        boff += static_cast<int64_t>(kc) * rp;   // a multiple of 16 floats
+        ++u;
+      }
+    }
+    g += tiles;
+  }
+  f.ubase[n] = u;
+  sc.n_units = u;
+  plan->part_b_floats = boff;
+  plan->part_h_floats = nc > 1 ? static_cast<int64_t>(nc) * pack->total_tokens * 64 : 0;
+  return (plan->part_b_floats + plan->part_h_floats) * 4 + 256;
+}
+
+static int run_dual(cudaStream_t st, const plora_pack_t* pack, int64_t k, const DualPlan& plan, const void* dY,
+                    const void* Bt_sh, const void* Hs, void* dH, float* gradB, void* ws) {
+  const int64_t T = pack->total_tokens;
+  DualArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc;
+  if ((rc = make_map_2d(&a.tmY, dY, k, T, k, 64, kBM))) return rc;
+  if ((rc = make_map_3d(&a.tmL, Bt_sh, 64, k, pack->n_adapters, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmH, Hs, 64, T, 64, 64, kBM))) return rc;
+  float* part_b = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  a.mtiles = pack->d_mtiles;
+  a.alpha = pack->d_alpha;
+  a.rpad_off = pack->d_rpad_off;
+  a.dH = static_cast<__nv_bfloat16*>(dH);
+  a.part_b = part_b;
+  a.part_h = part_b + plan.part_b_floats;
+  a.T = T;
+  static std::atomic<uint64_t> configured{0};
+  if (ensure_smem(plora_dual_kernel, kDualSmemBytes, configured)) return 1;
+  const int grid = plan.sched.n_units < num_sms() ? plan.sched.n_units : num_sms();
+  plora_dual_kernel<<<grid, 192, kDualSmemBytes, st>>>(a, plan.sched);
+  PLORA_CUDA(cudaGetLastError());
+  DualFix f = plan.fix;
+  const int64_t g4 = gradB ? (k * pack->rpad16_total + 3) / 4 : 0;   // float4s of the dB^T region
+  f.nb_b = static_cast<int>((g4 + 255) / 256);
+  const int nb_h = plan.sched.nc > 1 ? pack->n_mtiles : 0;
+  if (f.nb_b + nb_h > 0) {
+    plora_dual_fix_kernel<<<f.nb_b + nb_h, 256, 0, st>>>(f, plan.sched, part_b, a.part_h, pack->d_rpad_off,
+                                                        pack->d_alpha, pack->d_mtiles, T, gradB,
+                                                        static_cast<__nv_bfloat16*>(dH));
+    PLORA_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
 extern "C" {
 
 int plora_abi_version(void) { return PLORA_ABI_VERSION; }
@@ -754,6 +851,31 @@ int plora_lora_shrink_multi(void* stream, const plora_pack_t* pack, int64_t K, c
     return 0;
   }
   return run_shrink_multi(static_cast<cudaStream_t>(stream), pack, K, P, n_multi, L_sh, outs);
+}
+
+int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off) {
+  if (check_pack(pack)) return -1;
+  auto plan = std::make_unique<DualPlan>();
+  const int64_t b = dual_plan(pack, k, h_rpad_off, plan.get());
+  return b < 0 ? 0 : b;
+}
+
+int plora_lora_dual(void* stream, const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, const void* dY,
+                    const void* Bt_sh, const void* Hs, void* dH, float* gradB, void* ws, int64_t ws_bytes) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (!dY || !Bt_sh || !dH || (gradB && !Hs)) return fail("lora_dual: NULL operand");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pack->total_tokens > 0 && pack->n_mtiles > 0) {
+    auto plan = std::make_unique<DualPlan>();
+    const int64_t need = dual_plan(pack, k, h_rpad_off, plan.get());
+    if (need >= 0 && ws != nullptr && ws_bytes >= need)
+      return run_dual(st, pack, k, *plan, dY, Bt_sh, Hs, dH, gradB, ws);
+  }
+  // not eligible (or no workspace): the separate K4 / K3 kernels, same results up to fp32 association
+  if ((rc = run_shrink(st, pack, k, dY, Bt_sh, dH))) return rc;
+  if (gradB && (rc = run_segred(st, pack, k, dY, Hs, gradB))) return rc;
+  return 0;
 }
 
 int plora_lora_segred_multi(void* stream, const plora_pack_t* pack, int64_t Mdim, const void* P, int32_t n_multi,

@@ -211,7 +211,7 @@ class PackedLoraTrainer:
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
                  save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool = False,
-                 tp_chunks: int = 4, fuse_swiglu: bool = True):
+                 tp_chunks: int = 4, fuse_swiglu: bool = True, fuse_dual: bool = True):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
@@ -220,7 +220,8 @@ class PackedLoraTrainer:
         activation estimate leaves headroom on the device).  ``tp_chunks``: token chunks of
         the TP all-reduce / GEMM overlap; ``tp_fused``: row-parallel GEMMs reduce into the
         owner's buffer over peer memory (opt-in, unmeasured on NVLink); ``fuse_swiglu``:
-        gate/up GEMM with the SwiGLU forward in its epilogue."""
+        gate/up GEMM with the SwiGLU forward in its epilogue; ``fuse_dual``: K4 (dH) and K3
+        (dB) of every target in one pass over dY (ops.lora_dual) instead of two."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -269,6 +270,7 @@ class PackedLoraTrainer:
         self._peer = {}
         # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
         self._fuse_swiglu = self.targets[4].h_out >= 256 and fuse_swiglu
+        self._fuse_dual = bool(fuse_dual)
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
@@ -504,6 +506,18 @@ class PackedLoraTrainer:
         x.record_stream(side)
         return x, parts
 
+    def _dy_pass(self, layer: int, nm: str, dy: torch.Tensor, hs: torch.Tensor, dh: torch.Tensor) -> None:
+        """Cases 2 and 1 of the reference backward (lorapack.py:225, :224) for one target:
+        dH = alpha dY B^T into ``dh`` and dB^T = Hs^T dY into the grad region -- one fused
+        pass over dY (K4 + K3, ops.lora_dual) or the two separate kernels."""
+        bank, meta = self.bank, self.meta
+        bt, g = bank.shadow_of(layer, nm, "B"), bank.region_flat(bank.G, layer, nm, "B")
+        if self._fuse_dual and meta.nb == 1:
+            ops.lora_dual(meta, dy, bt, hs, dh, g)
+        else:
+            ops.shrink(meta, dy, bt, dh)        # K4 (Case 2)
+            ops.segred(meta, dy, hs, g)         # K3 (Case 1)
+
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
         """Backward of targets sharing the input x: per target K4 dH and K3 dB; ONE grouped
         K6 launch sums every target's input gradient in one fp32 accumulator; ONE K5
@@ -514,8 +528,7 @@ class PackedLoraTrainer:
         dhs = []
         for nm, hs, dy in zip(names, hss, dys):
             dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
-            ops.shrink(meta, dy, bank.shadow_of(layer, nm, "B"), dh)                        # K4 (Case 2)
-            ops.segred(meta, dy, hs, bank.region_flat(bank.G, layer, nm, "B"))              # K3 (Case 1)
+            self._dy_pass(layer, nm, dy, hs, dh)                                           # K4 + K3
             dhs.append(dh)
         dx = None
         ws, ashs = [lw[nm] for nm in names], [bank.shadow_of(layer, nm, "A") for nm in names]
@@ -607,8 +620,7 @@ class PackedLoraTrainer:
         dh_s = dh
         dh = self._gather(dh_s)   # sequence parallel: the row-parallel output gradient on all T rows
         dh_down = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
-        ops.shrink(meta, dh, bank.shadow_of(layer, "down", "B"), dh_down)                     # K4
-        ops.segred(meta, dh, sv.hs["down"], bank.region_flat(bank.G, layer, "down", "B"))    # K3
+        self._dy_pass(layer, "down", dh, sv.hs["down"], dh_down)                              # K4 + K3
         d_act = ops.linear_expand(meta, dh, lw["down"], False, bank.shadow_of(layer, "down", "A"), dh_down)  # K6
         del dh
         act = torch.empty_like(sv.g)

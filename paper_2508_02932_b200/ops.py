@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -235,6 +237,59 @@ def segred(meta: PackMeta, p: torch.Tensor, q: torch.Tensor, g: torch.Tensor) ->
         _TIMER.stop("segred", t, flops=2.0 * Mdim * tr, nbytes=2.0 * T * Mdim + 2.0 * tr + 4.0 * Mdim * R,
                     detail=f"M{Mdim}")
     return g
+
+
+_DUAL_WS: dict = {}
+
+
+def _dual_workspace(nbytes: int) -> torch.Tensor:
+    """Partials workspace of the fused K3 + K4 pass for the current (device, stream), grown
+    to the largest request (no zero-fill needed; launches on one stream are ordered)."""
+    dev = torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream().cuda_stream)
+    ws = _DUAL_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=f"cuda:{dev}")
+        _DUAL_WS[key] = ws
+    return ws
+
+
+def _h_rpad(meta: PackMeta):
+    if not hasattr(meta, "_h_rpad_c"):
+        meta._h_rpad_c = np.ascontiguousarray(meta.rpad_off, dtype=np.int32)
+    return meta._h_rpad_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def lora_dual(meta: PackMeta, dy: torch.Tensor, bt_sh: torch.Tensor, hs: torch.Tensor | None,
+              dh_out: torch.Tensor, g: torch.Tensor | None) -> torch.Tensor:
+    """K4 + K3 in one pass over dY (reference lorapack.py:224-225): dh_out = alpha_i dY_i B_i^T
+    (bf16 [T][rpad64]) and, when g is given, the dB_i^T grad region = Hs_i^T dY_i (fp32).
+    Packs too small to fill the SMs run the separate K4 / K3 kernels (plora_lora_dual)."""
+    T, k = dy.shape
+    _on_current_device(dy, "dy")
+    _lora_shapes(meta, k, bt_sh, dh_out, meta.total_tokens)
+    if g is not None:
+        _size(hs, "hs", meta.total_tokens * meta.rpad64)
+        _size(g, "g", k * meta.rpad16_total)
+    s = _pack(meta)
+    rp = _h_rpad(meta)
+    need = int(_lib.lib().plora_lora_dual_workspace_bytes(ctypes.byref(s), k, rp))
+    ws = _dual_workspace(need) if need > 0 else None
+    t = _TIMER.start() if _TIMER else None
+    _lib.check(_lib.lib().plora_lora_dual(_stream(), ctypes.byref(s), k, rp, _need(dy, "dy"), _need(bt_sh, "bt_sh"),
+                                          _need(hs, "hs", allow_none=g is None), _need(dh_out, "dh_out"),
+                                          _need(g, "g", torch.float32, allow_none=True),
+                                          ws.data_ptr() if ws is not None else None, need),
+               "plora_lora_dual")
+    _LAUNCHES[0] += 2 if g is not None else 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        if need > 0:
+            _TIMER.stop("dual", t, flops=4.0 * k * tr, nbytes=2.0 * T * k + 4.0 * tr + 6.0 * k * R, detail=f"K{k}")
+        else:   # separate K4 + K3 launches: both passes' algorithmic bytes
+            _TIMER.stop("dual", t, flops=4.0 * k * tr, nbytes=4.0 * T * k + 6.0 * tr + 6.0 * k * R,
+                        detail=f"K{k}sep")
+    return dh_out
 
 
 def _ptr_array(ts, name, dtype=torch.bfloat16):
