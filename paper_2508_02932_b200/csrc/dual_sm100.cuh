@@ -26,6 +26,13 @@
 
 namespace plora {
 
+#ifndef PLORA_DUAL_RANK_N
+// MMA N = the adapter's rpad16 instead of 64 (build-time knob): parity-green, but no faster
+// at C3 (K = 4096: 92.1 vs 90.2 us isolated, profiles/r2_dual_kernels.log) -- the kernel is
+// paced by the tensor pipe's per-MMA cost at K = 16 x N = 64, not by B-operand bytes
+#define PLORA_DUAL_RANK_N 0
+#endif
+
 constexpr int kDualRC = 4;                 // m-tiles per unit
 constexpr int kDualStages = 4;             // dY ring: [128 rows][128 cols] bf16 = 32 KB per stage
 constexpr int kDualMaxUnits = 3072;
@@ -157,8 +164,6 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_shrink = idesc_bf16(128, 64, false, true);
-    constexpr uint32_t idesc_red = idesc_bf16(128, 64, true, true);
     int st = 0, ls = 0, bb = 0;
     uint32_t ph = 0, lph = 0, hph = 0, bph = 0, dph = 0;
     for (int ui = blockIdx.x; ui < sched.n_units; ui += gridDim.x) {
@@ -167,6 +172,16 @@ __global__ void __launch_bounds__(192, 1)
       const int4* mt = reinterpret_cast<const int4*>(args.mtiles) + g0;
       const int col0 = c * kc;
       const int nsteps = (min(kc, k - col0)) / 128;
+#if PLORA_DUAL_RANK_N
+      // N = the adapter's rpad16 (16..64): fewer B-operand bytes read from shared memory
+      // per MMA -- the kernel is bound by shared-memory bandwidth (each staged dY byte is
+      // read by two MMAs); columns past rpad16 of D_h stay stale and are not stored
+      const uint32_t nr = static_cast<uint32_t>(args.rpad_off[mt[0].z + 1] - args.rpad_off[mt[0].z]);
+#else
+      const uint32_t nr = 64;
+#endif
+      const uint32_t idesc_shrink = idesc_bf16(128, nr, false, true);
+      const uint32_t idesc_red = idesc_bf16(128, nr, true, true);
       mbar_wait(&dhempty[0], dph ^ 1);   // D_h of the previous unit drained
       dph ^= 1;
       tc_fence_after();
@@ -281,8 +296,16 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem + 64 * j + h * 32 + lane_off, r);
-          tmem_ld_wait();
+          if (h * 32 < rp) {
+            tmem_ld_32x32b_x32(tmem + 64 * j + h * 32 + lane_off, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (h * 32 + q >= rp) r[q] = 0u;   // past rpad16: not computed (N = rpad16)
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) r[q] = 0u;
+          }
           if (!ok) continue;
           if (sched.nc == 1) {   // complete: alpha-scaled bf16 dH (zero past the rank: L is zero-padded)
             __nv_bfloat16* o = args.dH + t * 64 + h * 32;

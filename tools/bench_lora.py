@@ -59,7 +59,7 @@ def main():
         meta = build_meta(ranks, tokens, [1.0] * len(ranks)).to("cuda")
         T, R64 = meta.total_tokens, meta.rpad64
         tr, R = sum(t * r for t, r in zip(tokens, ranks)), sum(ranks)
-        for K in (4096, 14336):
+        for K in (1024, 4096, 14336):
             name = f"{pname}_K{K}"
             if only and only not in name:
                 continue
@@ -82,6 +82,10 @@ def main():
                     ops._pack = orig
                 row[mode] = {"shrink_us": round(t_sh * 1e3, 1), "shrink_gbs": round(sh_bytes / t_sh / 1e6),
                              "segred_us": round(t_sg * 1e3, 1), "segred_gbs": round(sg_bytes / t_sg / 1e6)}
+            dh = torch.empty(T, R64, device="cuda", dtype=bf)
+            t_du = timeit(lambda: ops.lora_dual(meta, p, l_sh, q, dh, g))
+            row["dual_us"] = round(t_du * 1e3, 1)
+            row["dual_gbs_equiv"] = round((sh_bytes + sg_bytes) / t_du / 1e6)   # the two separate passes' bytes
             out[name] = row
             print(name, json.dumps(row), flush=True)
     print(json.dumps({"lora_kernels": out, "peak_gbs": PEAK}))
