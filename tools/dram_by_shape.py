@@ -13,7 +13,10 @@ import json
 import sys
 from collections import OrderedDict
 
-TIMED = ("plora_gemm_pair_kernel", "plora_gemm_kernel", "plora_segred_lpt_kernel", "adamw_kernel")
+TIMED = ("plora_gemm_pair_kernel", "plora_gemm_kernel", "plora_segred_lpt_kernel", "adamw_kernel", "plora_dual")
+# launches per record: the fused K3+K4 pass is the dual kernel + its fix-up (or, for packs
+# too small for it, the separate shrink + segment reduction)
+PER_RECORD = {"dual": 2}
 UNITS = {"ns": 1.0, "nsecond": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
@@ -37,10 +40,18 @@ def launches(path):
 def main(lpath, rpath, out, traffic_out=None):
     ls = [(n, m) for n, m in launches(lpath) if any(k in n for k in TIMED)]
     recs = json.load(open(rpath))
-    if len(ls) != len(recs):
-        raise SystemExit(f"{len(ls)} timed-kernel launches in the ncu list but {len(recs)} bench records")
+    need = sum(PER_RECORD.get(r["kind"], 1) for r in recs)
+    if len(ls) != need:
+        raise SystemExit(f"{len(ls)} timed-kernel launches in the ncu list but {need} for the bench records")
+    pairs, i = [], 0
+    for r in recs:
+        k = PER_RECORD.get(r["kind"], 1)
+        grp = ls[i:i + k]
+        i += k
+        m = {key: sum(g[1].get(key, 0.0) for g in grp) for key in grp[0][1]}
+        pairs.append(((grp[0][0], m), r))
     agg = OrderedDict()
-    for (name, m), r in zip(ls, recs):
+    for (name, m), r in pairs:
         key = f"{r['kind']}[{r['detail']}]"
         a = agg.setdefault(key, {"launches": 0, "ncu_ms": 0.0, "dram_read": 0.0, "dram_write": 0.0,
                                  "algo_bytes": 0.0, "flops": 0.0, "kernel": name.split("(")[0]})

@@ -47,13 +47,20 @@ def time_job(cfg_name, idx, steps, warmup, kernels=False, graph=False):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     T = tr.T
-    if kernels and not graph:   # one more step with the per-launch timer: per kernel class ms / step
+    if kernels:   # per kernel class ms / step: the step captured with event-record nodes around every
+        # libplora launch (device times, no host gaps; as bench.py's kernel stats), one replay
         from paper_2508_02932_b200 import ops
-        timer = ops.KernelTimer()
+        timer = ops.KernelTimer(external=True)
         ops.set_timer(timer)
-        tr.step(tok)
-        ops.set_timer(None)
+        try:
+            tg = tr.graphed(tok, warmup=0)
+        finally:
+            ops.set_timer(None)
+        tg.step()
+        torch.cuda.synchronize()
+        tg.step()
         summ = timer.summary()
+        del tg
         print(json.dumps({"job": list(idx), "T": T, "ms_per_step": round(ms, 2), "host_ms_per_step": round(host_ms, 2),
                           "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 2)}
                                       for k, v in summ.items()}}), flush=True)
