@@ -682,11 +682,25 @@ static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t M
 using namespace plora;
 
 // ---------------------------------------------------------------- fused K3 + K4 (dual_sm100.cuh)
-// Plan of the one-dY-pass kernel for (pack, k): units of up to kDualRC 128-row m-tiles of
-// one adapter x nc column chunks.  nc grows (1, 2, 4) until the units cover 3/4 of the SMs;
-// a pack with fewer than half the SMs' worth of units (planner-split ranks at small T) or
-// with rank blocks > 1 / k not a multiple of 128 is not eligible (separate stream-K
-// kernels instead).  Returns the workspace bytes (partials) or -1 when not eligible.
+// Plan of the one-dY-pass kernel for (pack, k): units of rcs (1, 2 or 4) 128-row m-tiles of
+// one adapter x nc (1..8) column chunks of k.  The (rcs, nc) pair is chosen with a small
+// time model -- waves of units streaming dY at a per-SM rate, plus the fp32 partials'
+// round trip and the fix-up -- and compared against the two separate passes (two
+// launches' fixed cost + dY twice); the separate K4 / K3 kernels win for packs too small
+// to amortise the partials.  Nor is a pack eligible with rank blocks > 1 or k % 128 != 0.
+// Returns the workspace bytes (partials) or -1 when the separate kernels are used.
+#ifndef PLORA_DUAL_SM_GBS
+#define PLORA_DUAL_SM_GBS 40.0        // dY streaming rate of one CTA of the fused kernel (GB/s)
+#endif
+#ifndef PLORA_DUAL_HBM_GBS
+#define PLORA_DUAL_HBM_GBS 5000.0     // achieved HBM rate of the LoRA kernels (GB/s)
+#endif
+#ifndef PLORA_DUAL_LAUNCH_US
+#define PLORA_DUAL_LAUNCH_US 12.0     // fixed cost of one LoRA launch (fill, tail, launch gap)
+#endif
+#ifndef PLORA_DUAL_UNIT_US
+#define PLORA_DUAL_UNIT_US 2.0        // per-unit cost of the fused kernel (Hs load, D_h drain)
+#endif
 struct DualPlan {
   DualSched sched;
   DualFix fix;
@@ -699,15 +713,45 @@ static int64_t dual_plan(const plora_pack_t* pack, int64_t k, const int32_t* h_r
   if (!pack->h_row_off || !h_rpad_off || pack->nb != 1 || k <= 0 || k % 128 || n > kDualMaxAdapters ||
       k > (1 << 24))
     return -1;
-  int64_t chunks = 0;
-  for (int a = 0; a < n; ++a) {
-    const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
-    chunks += (tiles + kDualRC - 1) / kDualRC;
-  }
   const int sms = num_sms();
-  int nc = 1;
-  while (chunks * nc < sms * 3 / 4 && nc < 4 && k / 128 >= 2 * nc) nc *= 2;
-  if (chunks == 0 || chunks * nc < sms / 2 || chunks * nc > kDualMaxUnits) return -1;
+  const int64_t T = pack->total_tokens;
+  int64_t sum_rp = 0, tiles_all = 0;
+  for (int a = 0; a < n; ++a) {
+    const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
+    if (rp <= 0 || rp > 64) return -1;
+    const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
+    sum_rp += rp * tiles;   // sum over m-tiles of rpad16 (partials scale with it)
+    tiles_all += tiles;
+  }
+  if (tiles_all == 0) return -1;
+  const double avg_rp = static_cast<double>(sum_rp) / tiles_all;
+  const double sep_us = 2.0 * PLORA_DUAL_LAUNCH_US + 4.0 * T * k / (PLORA_DUAL_HBM_GBS * 1e3);
+  double best_us = sep_us;
+  int best_rcs = 0, best_nc = 0;
+  for (int rcs : {4, 2, 1}) {
+    int64_t chunks = 0;
+    for (int a = 0; a < n; ++a) {
+      const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
+      chunks += (tiles + rcs - 1) / rcs;
+    }
+    for (int nc = 1; nc <= 8 && k / 128 >= nc; nc *= 2) {
+      const int64_t units = chunks * nc;
+      if (units > kDualMaxUnits) break;
+      const int64_t kc = ((k + nc - 1) / nc + 127) / 128 * 128;
+      const int64_t waves = (units + sms - 1) / sms;
+      const double unit_us = rcs * 128.0 * kc * 2 / (PLORA_DUAL_SM_GBS * 1e3) + PLORA_DUAL_UNIT_US;
+      const double part_bytes = 4.0 * avg_rp * (static_cast<double>(chunks) * k + (nc > 1 ? nc * static_cast<double>(T) : 0.0));
+      const double us = waves * unit_us + 2.0 * part_bytes / (PLORA_DUAL_HBM_GBS * 1e3) + PLORA_DUAL_LAUNCH_US;
+      if (us < best_us) {
+        best_us = us;
+        best_rcs = rcs;
+        best_nc = nc;
+      }
+    }
+  }
+  if (best_rcs == 0) return -1;
+  const int rcs = best_rcs;
+  int nc = best_nc;
   const int kc = static_cast<int>(((k + nc - 1) / nc + 127) / 128 * 128);
   nc = static_cast<int>((k + kc - 1) / kc);
   DualSched& sc = plan->sched;
@@ -723,8 +767,8 @@ static int64_t dual_plan(const plora_pack_t* pack, int64_t k, const int32_t* h_r
     const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
     const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
     if (rp <= 0 || rp > 64) return -1;
-    for (int64_t q = 0; q < tiles; q += kDualRC) {
-      const int rc = static_cast<int>(tiles - q < kDualRC ? tiles - q : kDualRC);
+    for (int64_t q = 0; q < tiles; q += rcs) {
+      const int rc = static_cast<int>(tiles - q < rcs ? tiles - q : rcs);
       if (g + q >= (1 << 20)) return -1;
       for (int c = 0; c < nc; ++c) {
         sc.unit[u] = static_cast<uint32_t>(g + q) | static_cast<uint32_t>(rc - 1) << 20 | static_cast<uint32_t>(c) << 22;

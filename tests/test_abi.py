@@ -52,8 +52,8 @@ def test_invalid_arguments_return_status_and_message():
 def test_fused_dy_pass_plan_on_host():
     """plora_lora_dual_workspace_bytes plans the fused K3+K4 pass on the host (no device
     memory is touched): the C3 pack (16 adapters, T = 32768) takes the fused path with
-    fp32 partials of about a third of dY's bytes; a planner-split rank's pack (one
-    adapter, T = 4096: 8 row chunks) and rank blocks > 1 run the separate kernels (0)."""
+    fp32 partials of about a third of dY's bytes; rank blocks > 1 and k % 128 != 0 run
+    the separate kernels (0)."""
     import ctypes
 
     import numpy as np
@@ -78,7 +78,6 @@ def test_fused_dy_pass_plan_on_host():
     ws, meta = plan([8, 16, 32, 64] * 4, c3_tokens, 4096)
     dy_bytes = 2 * meta.total_tokens * 4096
     assert 0.15 * dy_bytes < ws < 0.5 * dy_bytes, (ws, dy_bytes)
-    assert plan([64], [4096], 4096)[0] == 0          # too few units for the SMs
     assert plan([8, 100], [4096, 4096], 4096)[0] == 0  # rank > 64: two rank blocks
     assert plan([8, 16, 32, 64] * 4, c3_tokens, 4000)[0] == 0   # k not a multiple of 128
     assert np.all(np.diff(meta.rpad_off) % 16 == 0)

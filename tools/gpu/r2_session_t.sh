@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python tools/split_projection.py --gpus 8 --steps 5 --warmup 2 --graph --kernels > gpurun_out/r2t_split8_kernels.log 2>&1; echo rc=$?
+python - <<'PY'
+import json
+for line in open('gpurun_out/r2t_split8_kernels.log'):
+    if line.startswith('{"job"'):
+        d = json.loads(line); k = d['kernels']
+        print(d['job'], d['T'], d['ms_per_step'], {x: k[x]['ms'] for x in ('gemm','shrink','segred','dual','adamw') if x in k})
+PY
