@@ -579,6 +579,9 @@ def main() -> None:
         if d["bytes"]:
             kernels[kind]["hbm_gbs"] = round(d["bytes"] / sec / 1e9, 1)
             kernels[kind]["hbm_frac"] = round(d["bytes"] / sec / 1e9 / peaks["hbm_gbs"], 3)
+    if "dual" in kernels:
+        kernels["dual"]["note"] = ("K4+K3 fused: bytes = ONE pass over dY (the separate kernels stream it twice); "
+                                   "paced by the tensor pipe / smem operand reads, not DRAM (profiles/r2_lora_ncu.md)")
     useful = useful_flops(cfg, specs, s, tp) if specs else {"base": 0.0, "lora": 0.0, "attention": 0.0}
     useful_all = {k: sum_over_ranks(v) for k, v in useful.items()}   # this rank's share, summed
     per_rank = {"rank": rank, "device": device, "world": dist.get_world_size() if world > 1 else 1,

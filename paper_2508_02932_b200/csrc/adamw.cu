@@ -19,6 +19,7 @@
 #include <string>
 
 #include "../../include/plora.h"
+#include "pdl.cuh"
 
 namespace plora {
 int set_error(const std::string& msg);
@@ -34,6 +35,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(int64_t n_chunks, const long
                                                     __nv_bfloat16* __restrict__ shadow,
                                                     const float4* __restrict__ hp, float beta1,
                                                     float beta2, float eps, float bc1_all, float bc2_sqrt_all) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     const longlong4 ch = chunks[c];
     const int64_t p_off = ch.x;
@@ -105,7 +108,7 @@ extern "C" int plora_adamw(void* stream, int64_t n_chunks, const int64_t* chunks
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = static_cast<int64_t>(sms) * 8;
   const int grid = static_cast<int>(n_chunks < want ? n_chunks : want);
-  adamw_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(adamw_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       n_chunks, reinterpret_cast<const longlong4*>(chunks), param, grad, exp_avg, exp_avg_sq,
       static_cast<__nv_bfloat16*>(shadow), reinterpret_cast<const float4*>(hp), beta1, beta2, eps,
       static_cast<float>(bc1), static_cast<float>(sqrt(bc2)));

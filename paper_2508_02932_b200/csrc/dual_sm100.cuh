@@ -23,6 +23,7 @@
 // Hs tail masking, warps 2..5 epilogue (TMEM lane quarter = warp % 4).
 #pragma once
 #include "sm100.cuh"
+#include "pdl.cuh"
 
 namespace plora {
 
@@ -123,6 +124,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -362,6 +365,8 @@ __global__ void __launch_bounds__(256) plora_dual_fix_kernel(const __grid_consta
                                                              const float* __restrict__ alpha,
                                                              const int32_t* __restrict__ mtiles, int64_t T,
                                                              float* __restrict__ G, __nv_bfloat16* __restrict__ dH) {
+  pdl_wait();
+  pdl_trigger();
   if (static_cast<int>(blockIdx.x) < f.nb_b) {
     const int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;   // element of G
     const int64_t k = f.k;

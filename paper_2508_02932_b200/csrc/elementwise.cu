@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/plora.h"
+#include "pdl.cuh"
 
 namespace plora {
 int set_error(const std::string& msg);
@@ -61,6 +62,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_fwd_kernel(const bf16* _
                                                                    bf16* __restrict__ y,
                                                                    float* __restrict__ rstd, int d,
                                                                    float eps, int use_given) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
   const bf16* xr = x + row * d;
@@ -102,6 +105,8 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(const bf16* _
                                                                    const bf16* __restrict__ w,
                                                                    bf16* __restrict__ sum, bf16* __restrict__ y,
                                                                    float* __restrict__ rstd, int d, float eps) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
   float v[kMaxV][8];
@@ -147,6 +152,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* _
                                                                    const bf16* __restrict__ w,
                                                                    const bf16* __restrict__ res,
                                                                    bf16* __restrict__ dx, int d) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
   const float r = rstd[row];
@@ -185,6 +192,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(const bf16* _
 // ---------------------------------------------------------------- SwiGLU
 __global__ void swiglu_fwd_kernel(const bf16* __restrict__ g, const bf16* __restrict__ u,
                                   bf16* __restrict__ a, int64_t n8) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     float gf[8], uf[8], o[8];
     load8(g + i * 8, gf);
@@ -198,6 +207,8 @@ __global__ void swiglu_fwd_kernel(const bf16* __restrict__ g, const bf16* __rest
 __global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* g, const bf16* u, bf16* dg,
                                   bf16* du, bf16* __restrict__ act,
                                   int64_t n8) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     float af[8], gf[8], uf[8], og[8], ou[8];
     load8(da + i * 8, af);
@@ -228,6 +239,8 @@ __global__ void rope_kernel(const bf16* __restrict__ in, bf16* __restrict__ out,
                             const float* __restrict__ cosv, const float* __restrict__ sinv, int64_t T,
                             int s, int H, int hd, int64_t sb, int64_t sp, int64_t sh, int rotate,
                             float sign) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   const int half = hd / 2;
   const int per_head = half / 8;
   const int64_t total = T * H * per_head;
@@ -269,6 +282,8 @@ constexpr int kCeThreads = 512;
 __global__ void __launch_bounds__(kCeThreads) ce_kernel(bf16* __restrict__ logits, const int64_t* __restrict__ labels,
                                                         const float* __restrict__ weight,
                                                         float* __restrict__ tok_loss, int V) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   __shared__ float red[kCeThreads / 32];
   __shared__ float redm[kCeThreads / 32];
   const int64_t row = blockIdx.x;
@@ -348,6 +363,8 @@ __global__ void __launch_bounds__(kCeThreads) ce_kernel(bf16* __restrict__ logit
 __global__ void __launch_bounds__(kCeThreads) ce_stats_kernel(const bf16* __restrict__ logits,
                                                               const int64_t* __restrict__ labels,
                                                               float* __restrict__ stats, int V, int64_t v0) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   __shared__ float red[kCeThreads / 32];
   __shared__ float redm[kCeThreads / 32];
   const int64_t row = blockIdx.x;
@@ -398,6 +415,8 @@ __global__ void __launch_bounds__(kCeThreads) ce_stats_kernel(const bf16* __rest
 __global__ void ce_apply_kernel(bf16* __restrict__ logits, const int64_t* __restrict__ labels,
                                 const float* __restrict__ lse, const float* __restrict__ weight, int V,
                                 int64_t v0) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   const int64_t row = blockIdx.x;
   bf16* x = logits + row * (int64_t)V;
   const float w = weight[row];
@@ -417,6 +436,8 @@ __global__ void ce_apply_kernel(bf16* __restrict__ logits, const int64_t* __rest
 // y[r][c] = bf16(float(y[r][c]) + float(bias[c])) -- a broadcast row bias (narrow q/k/v shards).
 __global__ void add_row_bias_kernel(bf16* __restrict__ y, const bf16* __restrict__ bias, int64_t rows, int64_t n,
                                     int64_t ldy) {
+  plora::pdl_wait();
+  plora::pdl_trigger();
   const int64_t per = n / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * per; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / per, c = (i - r * per) * 8;
@@ -456,7 +477,7 @@ PLORA_API int plora_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const voi
                                 float eps, void* y, float* rstd, int32_t use_given_rstd) {
   if (d % 8 || d > 8 * kNormThreads * kMaxV) return plora::set_error("rmsnorm: d must be a multiple of 8, <= 8192");
   if (rows <= 0) return 0;
-  rmsnorm_fwd_kernel<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(rmsnorm_fwd_kernel, dim3(rows), dim3(kNormThreads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), static_cast<const bf16*>(w), static_cast<bf16*>(y), rstd, (int)d, eps,
       use_given_rstd);
   return launch_status("rmsnorm_fwd");
@@ -466,7 +487,7 @@ PLORA_API int plora_add_rmsnorm_fwd(void* stream, int64_t rows, int64_t d, const
                                     const void* w, float eps, void* sum, void* y, float* rstd) {
   if (d % 8 || d > 8 * kNormThreads * kMaxV) return plora::set_error("rmsnorm: d must be a multiple of 8, <= 8192");
   if (rows <= 0) return 0;
-  add_rmsnorm_kernel<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(add_rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(a), static_cast<const bf16*>(b), static_cast<const bf16*>(w), static_cast<bf16*>(sum),
       static_cast<bf16*>(y), rstd, (int)d, eps);
   return launch_status("add_rmsnorm_fwd");
@@ -478,7 +499,7 @@ PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const voi
   if (rows <= 0) return 0;
   auto kern = d <= 8 * kNormThreads ? rmsnorm_bwd_kernel<1>
             : (d <= 16 * kNormThreads ? rmsnorm_bwd_kernel<2> : rmsnorm_bwd_kernel<kMaxV>);
-  kern<<<rows, kNormThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(kern, dim3(rows), dim3(kNormThreads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(dy), static_cast<const bf16*>(x), rstd, static_cast<const bf16*>(w),
       static_cast<const bf16*>(residual), static_cast<bf16*>(dx), (int)d);
   return launch_status("rmsnorm_bwd");
@@ -486,7 +507,7 @@ PLORA_API int plora_rmsnorm_bwd(void* stream, int64_t rows, int64_t d, const voi
 
 PLORA_API int plora_swiglu_fwd(void* stream, int64_t n, const void* g, const void* u, void* a) {
   if (n % 8) return plora::set_error("swiglu: n must be a multiple of 8");
-  swiglu_fwd_kernel<<<grid_for(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(swiglu_fwd_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(g), static_cast<const bf16*>(u), static_cast<bf16*>(a), n / 8);
   return launch_status("swiglu_fwd");
 }
@@ -494,7 +515,7 @@ PLORA_API int plora_swiglu_fwd(void* stream, int64_t n, const void* g, const voi
 PLORA_API int plora_swiglu_bwd(void* stream, int64_t n, const void* da, const void* g, const void* u, void* dg,
                                void* du, void* act) {
   if (n % 8) return plora::set_error("swiglu: n must be a multiple of 8");
-  swiglu_bwd_kernel<<<grid_for(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(swiglu_bwd_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(da), static_cast<const bf16*>(g), static_cast<const bf16*>(u),
       static_cast<bf16*>(dg), static_cast<bf16*>(du), static_cast<bf16*>(act), n / 8);
   return launch_status("swiglu_bwd");
@@ -506,7 +527,7 @@ PLORA_API int plora_rope(void* stream, const void* in, void* out, const float* c
   if (hd % 16) return plora::set_error("rope: head_dim must be a multiple of 16");
   if ((sb | sp | sh) % 8) return plora::set_error("rope: strides must be multiples of 8 elements");
   const int64_t total = T * H * (hd / 16);
-  rope_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(rope_kernel, dim3(grid_for(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(in), static_cast<bf16*>(out), cosv, sinv, T, s, H, hd, sb, sp, sh, rotate,
       inverse ? -1.f : 1.f);
   return launch_status("rope");
@@ -516,7 +537,7 @@ PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* l
                                   const float* weight, float* tok_loss) {
   if (rows <= 0) return 0;
   if ((V * 2) % 16) return plora::set_error("cross_entropy: V must be a multiple of 8");
-  ce_kernel<<<rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(ce_kernel, dim3(rows), dim3(kCeThreads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<bf16*>(logits), labels, weight, tok_loss, (int)V);
   return launch_status("cross_entropy");
 }
@@ -524,7 +545,7 @@ PLORA_API int plora_cross_entropy(void* stream, int64_t rows, int64_t V, void* l
 PLORA_API int plora_add_row_bias(void* stream, int64_t rows, int64_t n, void* y, int64_t ldy, const void* bias) {
   if (rows <= 0 || n <= 0) return 0;
   if (n % 8 || ldy % 8) return plora::set_error("add_row_bias: n and ldy must be multiples of 8");
-  add_row_bias_kernel<<<grid_for(rows * (n / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(add_row_bias_kernel, dim3(grid_for(rows * (n / 8), 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<bf16*>(y), static_cast<const bf16*>(bias), rows, n, ldy);
   return launch_status("add_row_bias");
 }
@@ -533,7 +554,7 @@ PLORA_API int plora_ce_stats(void* stream, int64_t rows, int64_t V, const void* 
                              int64_t v0, float* stats) {
   if (rows <= 0) return 0;
   if (V % 8) return plora::set_error("ce_stats: V must be a multiple of 8");
-  ce_stats_kernel<<<rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  plora::launch_pdl(ce_stats_kernel, dim3(rows), dim3(kCeThreads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(logits), labels, stats, (int)V, v0);
   return launch_status("ce_stats");
 }
@@ -542,7 +563,7 @@ PLORA_API int plora_ce_apply(void* stream, int64_t rows, int64_t V, void* logits
                              int64_t v0, const float* lse, const float* weight) {
   if (rows <= 0) return 0;
   if (V % 8) return plora::set_error("ce_apply: V must be a multiple of 8");
-  ce_apply_kernel<<<rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<bf16*>(logits), labels, lse,
+  plora::launch_pdl(ce_apply_kernel, dim3(rows), dim3(256), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(logits), labels, lse,
                                                                      weight, (int)V, v0);
   return launch_status("ce_apply");
 }

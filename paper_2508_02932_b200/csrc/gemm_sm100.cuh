@@ -21,6 +21,7 @@
 // TMA with 128-byte swizzle; UMMA reads them through shared-memory descriptors.
 #pragma once
 #include "sm100.cuh"
+#include "pdl.cuh"
 
 namespace plora {
 
@@ -413,6 +414,8 @@ __device__ __forceinline__ void gemm_body(const GemmArgs& args, const SegSched* 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();   // the next kernel may launch and run its prologue under this one's tail
+  pdl_wait();      // ... and this one touches global memory only after the previous grid completed
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -953,6 +956,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThread
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)

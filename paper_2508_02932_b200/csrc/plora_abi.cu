@@ -228,7 +228,7 @@ static int launch_as(const GemmArgs& args, cudaStream_t stream) {
   const int total = args.n_groups * args.n_ntiles;
   if (total <= 0) return 0;
   const int grid = SK ? args.sk : (total < num_sms() ? total : num_sms());
-  kern<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(args);
+  PLORA_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, args));
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
@@ -269,7 +269,8 @@ static int launch_pair(const PairArgs& args, cudaStream_t stream) {
   if (total <= 0) return 0;
   const int max_clusters = num_sms() / 2;
   const int clusters = total < max_clusters ? total : max_clusters;
-  kern<<<clusters * 2, PairCfg<NB, EPI>::kThreads, PairCfg<NB, EPI>::kSmemBytes, stream>>>(args);
+  PLORA_CUDA(launch_pdl(kern, dim3(clusters * 2), dim3(PairCfg<NB, EPI>::kThreads), PairCfg<NB, EPI>::kSmemBytes,
+                        stream, args));
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
@@ -573,7 +574,7 @@ static int launch_segred_lpt(const GemmArgs& args, const SegSched& sched, cudaSt
   auto kern = plora_segred_lpt_kernel<BN>;
   static std::atomic<uint64_t> configured{0};   // per instantiation, bit per device
   if (ensure_smem(kern, Cfg::kSmemBytes, configured)) return 1;
-  kern<<<sched.n_ctas, kThreads, Cfg::kSmemBytes, stream>>>(args, sched);
+  PLORA_CUDA(launch_pdl(kern, dim3(sched.n_ctas), dim3(kThreads), Cfg::kSmemBytes, stream, args, sched));
   PLORA_CUDA(cudaGetLastError());
   return 0;
 }
@@ -806,16 +807,17 @@ static int run_dual(cudaStream_t st, const plora_pack_t* pack, int64_t k, const 
   static std::atomic<uint64_t> configured{0};
   if (ensure_smem(plora_dual_kernel, kDualSmemBytes, configured)) return 1;
   const int grid = plan.sched.n_units < num_sms() ? plan.sched.n_units : num_sms();
-  plora_dual_kernel<<<grid, 192, kDualSmemBytes, st>>>(a, plan.sched);
+  PLORA_CUDA(launch_pdl(plora_dual_kernel, dim3(grid), dim3(192), kDualSmemBytes, st, a, plan.sched));
   PLORA_CUDA(cudaGetLastError());
   DualFix f = plan.fix;
   const int64_t g4 = gradB ? (k * pack->rpad16_total + 3) / 4 : 0;   // float4s of the dB^T region
   f.nb_b = static_cast<int>((g4 + 255) / 256);
   const int nb_h = plan.sched.nc > 1 ? pack->n_mtiles : 0;
   if (f.nb_b + nb_h > 0) {
-    plora_dual_fix_kernel<<<f.nb_b + nb_h, 256, 0, st>>>(f, plan.sched, part_b, a.part_h, pack->d_rpad_off,
-                                                        pack->d_alpha, pack->d_mtiles, T, gradB,
-                                                        static_cast<__nv_bfloat16*>(dH));
+    PLORA_CUDA(launch_pdl(plora_dual_fix_kernel, dim3(f.nb_b + nb_h), dim3(256), 0, st, f, plan.sched,
+                          static_cast<const float*>(part_b), static_cast<const float*>(a.part_h),
+                          pack->d_rpad_off, pack->d_alpha, pack->d_mtiles, T, gradB,
+                          static_cast<__nv_bfloat16*>(dH)));
     PLORA_CUDA(cudaGetLastError());
   }
   return 0;

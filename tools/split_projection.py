@@ -36,7 +36,8 @@ def time_job(cfg_name, idx, steps, warmup, kernels=False, graph=False):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     import time
-    run = tr.graphed(tok, warmup=1).step if graph else (lambda: tr.step(tok))
+    gs = tr.graphed(tok, warmup=1) if graph else None
+    run = gs.step if graph else (lambda: tr.step(tok))
     torch.cuda.synchronize()
     e0.record()
     h0 = time.perf_counter()
@@ -47,6 +48,8 @@ def time_job(cfg_name, idx, steps, warmup, kernels=False, graph=False):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     T = tr.T
+    del run, gs   # the timer graph below needs the memory of the step graph's pool
+    torch.cuda.empty_cache()
     if kernels:   # per kernel class ms / step: the step captured with event-record nodes around every
         # libplora launch (device times, no host gaps; as bench.py's kernel stats), one replay
         from paper_2508_02932_b200 import ops
