@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 7
+#define PLORA_ABI_VERSION 8
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -133,6 +133,16 @@ PLORA_API int plora_lora_shrink(void* stream, const plora_pack_t* pack, int64_t 
  * written into the adapter-major region G (P bf16 [T][Mdim], Q bf16 [T][rpad64]). */
 PLORA_API int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t Mdim,
                      const void* P, const void* Q, float* G);
+
+/* SwiGLU backward + K5 of the down projection in ONE pass (reference lorapack.py:226 for the
+ * down target, whose input is act = silu(g) * u):
+ *   dg = d_act * u * s (1 + g (1 - s)), du = d_act * g * s   (bf16 [T][ffn]; may alias g / u)
+ *   gradA region (down) = dA_i = act_i^T dH_i per segment    (f32, as plora_lora_segred with P = act)
+ * act is formed in shared memory and never written; results bit-identical to plora_swiglu_bwd
+ * followed by plora_lora_segred.  d_act, g, u bf16 [T][ffn]; dH bf16 [T][64].  Needs nb == 1
+ * and the pack's host row offsets (tile schedule). */
+PLORA_API int plora_swiglu_bwd_segred(void* stream, const plora_pack_t* pack, int64_t ffn, const void* d_act,
+                    const void* g, const void* u, const void* dH, void* dg, void* du, float* gradA);
 
 /* K4 + K3 in ONE pass over dY (reference lorapack.py:224-225, Cases 2 and 1):
  *   dH[T][64]      = alpha_i * dY_i B_i^T           (bf16, as plora_lora_shrink with L = Bt_sh)

@@ -32,6 +32,7 @@ EXPORTS = (
     "plora_lora_segred_multi",
     "plora_lora_dual_workspace_bytes",
     "plora_lora_dual",
+    "plora_swiglu_bwd_segred",
     "plora_linear_expand",
     "plora_linear_expand_group",
     "plora_add_row_bias",
@@ -58,7 +59,7 @@ EXPORTS = (
     "plora_tp_broadcast",
 )
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 
 class PloraError(RuntimeError):
@@ -118,6 +119,8 @@ _SIGNATURES = {
     "plora_lora_dual_workspace_bytes": ([ctypes.POINTER(PackStruct), _i64, _p32], _i64),
     "plora_lora_dual": ([_vp, ctypes.POINTER(PackStruct), _i64, _p32, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
                         ctypes.c_int),
+    "plora_swiglu_bwd_segred": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                                ctypes.c_int),
     "plora_linear_expand": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i64, _vp, _i32, _vp, _vp,
                              _vp, _i64, _vp], ctypes.c_int),
     "plora_linear_expand_group": ([_vp, ctypes.POINTER(PackStruct), _vp, _i64, _i32, _p64, ctypes.POINTER(_vp),

@@ -13,7 +13,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libplora.so"
 
 SOURCES = ["plora_abi.cu", "adamw.cu", "elementwise.cu", "meta.cpp", "tp_nccl.cpp"]
-HEADERS = ["sm100.cuh", "gemm_sm100.cuh"]
+HEADERS = ["sm100.cuh", "gemm_sm100.cuh", "dual_sm100.cuh", "swiglu_sm100.cuh", "swiglu_math.cuh", "pdl.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

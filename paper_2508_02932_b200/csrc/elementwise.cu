@@ -10,6 +10,7 @@
 
 #include "../../include/plora.h"
 #include "pdl.cuh"
+#include "swiglu_math.cuh"
 
 namespace plora {
 int set_error(const std::string& msg);
@@ -199,7 +200,7 @@ __global__ void swiglu_fwd_kernel(const bf16* __restrict__ g, const bf16* __rest
     load8(g + i * 8, gf);
     load8(u + i * 8, uf);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = gf[e] / (1.f + __expf(-gf[e])) * uf[e];
+    for (int e = 0; e < 8; ++e) o[e] = plora::swiglu_act(gf[e], uf[e]);
     store8(a + i * 8, o);
   }
 }
@@ -210,22 +211,13 @@ __global__ void swiglu_bwd_kernel(const bf16* __restrict__ da, const bf16* g, co
   plora::pdl_wait();
   plora::pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    float af[8], gf[8], uf[8], og[8], ou[8];
+    float af[8], gf[8], uf[8], og[8], ou[8], oa[8];
     load8(da + i * 8, af);
     load8(g + i * 8, gf);
     load8(u + i * 8, uf);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float s = 1.f / (1.f + __expf(-gf[e]));
-      ou[e] = af[e] * gf[e] * s;
-      og[e] = af[e] * uf[e] * s * (1.f + gf[e] * (1.f - s));
-    }
-    if (act) {   // same arithmetic as swiglu_fwd_kernel: bit-identical activation
-      float a[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = gf[e] / (1.f + __expf(-gf[e])) * uf[e];
-      store8(act + i * 8, a);
-    }
+    for (int e = 0; e < 8; ++e) plora::swiglu_bwd_elem(af[e], gf[e], uf[e], og[e], ou[e], oa[e]);
+    if (act) store8(act + i * 8, oa);   // the arithmetic of swiglu_fwd: bit-identical activation
     store8(dg + i * 8, og);
     store8(du + i * 8, ou);
   }

@@ -22,6 +22,7 @@
 #pragma once
 #include "sm100.cuh"
 #include "pdl.cuh"
+#include "swiglu_math.cuh"
 
 namespace plora {
 
@@ -691,6 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 #ifndef PLORA_STORE_EVICT_FIRST
 #define PLORA_STORE_EVICT_FIRST 0   // pair-epilogue TMA stores with an L2 evict_first policy (experiment knob)
 #endif
+#ifndef PLORA_PAIR_MAXNREG
+#define PLORA_PAIR_MAXNREG 0     // > 0: register cap of the pair kernel instead of launch_bounds(320, 1) (-> 168)
+#endif
+#if PLORA_PAIR_MAXNREG > 0
+#define PLORA_PAIR_BOUNDS __maxnreg__(PLORA_PAIR_MAXNREG)
+#else
+#define PLORA_PAIR_BOUNDS __launch_bounds__(PairCfg<NB>::kThreads, 1)
+#endif
 #ifndef PLORA_SWIGLU_DIRECT
 #define PLORA_SWIGLU_DIRECT 2       // SwiGLU epilogue: gate/up chunk pairs stored before the accumulator release
 #endif
@@ -901,7 +910,7 @@ __device__ __forceinline__ void pair_emit_swiglu(const PairOut& pg, const PairOu
   for (int q = 0; q < 16; ++q) {
     const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vg[q]));
     const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vu[q]));
-    va[q] = pack_bf16x2(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+    va[q] = pack_bf16x2(swiglu_act(g.x, u.x), swiglu_act(g.y, u.y));
   }
   pair_emit_chunk<NBUF>(pg, stg, issued, lane, col0, m0, m_len, vg);
   pair_emit_chunk<NBUF>(pu, stg, issued, lane, col0, m0, m_len, vu);
@@ -909,7 +918,7 @@ __device__ __forceinline__ void pair_emit_swiglu(const PairOut& pg, const PairOu
 }
 
 template <bool B_MN, int NB, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<NB>::kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) PLORA_PAIR_BOUNDS
     plora_gemm_pair_kernel(const __grid_constant__ PairArgs p) {
   using Cfg = PairCfg<NB, EPI>;
   const GemmArgs& args = p.g;

@@ -22,6 +22,7 @@
 #include "../../include/plora.h"
 #include "gemm_sm100.cuh"
 #include "dual_sm100.cuh"
+#include "swiglu_sm100.cuh"
 
 namespace plora {
 
@@ -682,6 +683,37 @@ static int run_segred_multi(cudaStream_t st, const plora_pack_t* pack, int64_t M
 
 using namespace plora;
 
+// ---------------------------------------------------------------- SwiGLU backward + K5 of down (swiglu_sm100.cuh)
+static int run_swiglu_segred(cudaStream_t st, const plora_pack_t* pack, int64_t ffn, const void* d_act,
+                             const void* g, const void* u, const void* dH, void* dg, void* du, float* G) {
+  const int64_t T = pack->total_tokens;
+  const int64_t Tm = T > 0 ? T : 1;
+  SwArgs a;
+  memset(&a, 0, sizeof(a));
+  int rc;
+  if ((rc = make_map_2d(&a.tmD, d_act, ffn, Tm, ffn, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmG, g, ffn, Tm, ffn, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmU, u, ffn, Tm, ffn, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmQ, dH, 64, Tm, 64, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmDG, dg, ffn, Tm, ffn, 64, 64))) return rc;
+  if ((rc = make_map_2d(&a.tmDU, du, ffn, Tm, ffn, 64, 64))) return rc;
+  a.dg = static_cast<__nv_bfloat16*>(dg);
+  a.du = static_cast<__nv_bfloat16*>(du);
+  a.row_off = pack->d_row_off;
+  a.rpad_off = pack->d_rpad_off;
+  a.out = G;
+  a.ffn = ffn;
+  a.M = static_cast<int>(ffn);
+  a.mt_per = static_cast<int>((ffn + kBM - 1) / kBM);
+  a.n_groups = pack->n_adapters * a.mt_per;
+  SegSched sched;
+  if (!segred_schedule(pack, a.mt_per, 1, &sched)) return fail("swiglu_bwd_segred: no tile schedule (host row offsets missing or too many tiles)");
+  static std::atomic<uint64_t> configured{0};
+  if (ensure_smem(plora_swiglu_segred_kernel, kSwSmemBytes, configured)) return 1;
+  PLORA_CUDA(launch_pdl(plora_swiglu_segred_kernel, dim3(sched.n_ctas), dim3(kSwThreads), kSwSmemBytes, st, a, sched));
+  return 0;
+}
+
 // ---------------------------------------------------------------- fused K3 + K4 (dual_sm100.cuh)
 // Plan of the one-dY-pass kernel for (pack, k): units of rcs (1, 2 or 4) 128-row m-tiles of
 // one adapter x nc (1..8) column chunks of k.  The (rcs, nc) pair is chosen with a small
@@ -897,6 +929,16 @@ int plora_lora_shrink_multi(void* stream, const plora_pack_t* pack, int64_t K, c
     return 0;
   }
   return run_shrink_multi(static_cast<cudaStream_t>(stream), pack, K, P, n_multi, L_sh, outs);
+}
+
+int plora_swiglu_bwd_segred(void* stream, const plora_pack_t* pack, int64_t ffn, const void* d_act, const void* g,
+                            const void* u, const void* dH, void* dg, void* du, float* gradA) {
+  int rc;
+  if ((rc = check_pack(pack))) return rc;
+  if (!d_act || !g || !u || !dH || !dg || !du || !gradA) return fail("swiglu_bwd_segred: NULL operand");
+  if (ffn % 8) return fail("swiglu_bwd_segred: ffn must be a multiple of 8");
+  if (pack->nb != 1) return fail("swiglu_bwd_segred: rank blocks > 1 (use plora_swiglu_bwd + plora_lora_segred)");
+  return run_swiglu_segred(static_cast<cudaStream_t>(stream), pack, ffn, d_act, g, u, dH, dg, du, gradA);
 }
 
 int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off) {

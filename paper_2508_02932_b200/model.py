@@ -211,7 +211,8 @@ class PackedLoraTrainer:
                  base: BaseWeights | None = None, ce_chunk: int = 4096, adapter_seeds=None,
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
                  save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool = False,
-                 tp_chunks: int = 4, fuse_swiglu: bool = True, fuse_dual: bool = True):
+                 tp_chunks: int = 4, fuse_swiglu: bool = True, fuse_dual: bool = True,
+                 fuse_swiglu_bwd: bool = True):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
@@ -221,7 +222,9 @@ class PackedLoraTrainer:
         the TP all-reduce / GEMM overlap; ``tp_fused``: row-parallel GEMMs reduce into the
         owner's buffer over peer memory (opt-in, unmeasured on NVLink); ``fuse_swiglu``:
         gate/up GEMM with the SwiGLU forward in its epilogue; ``fuse_dual``: K4 (dH) and K3
-        (dB) of every target in one pass over dY (ops.lora_dual) instead of two."""
+        (dB) of every target in one pass over dY (ops.lora_dual) instead of two;
+        ``fuse_swiglu_bwd``: the SwiGLU backward and the down projection's dA in one kernel
+        (ops.swiglu_bwd_segred: the activation never goes to HBM)."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -271,6 +274,7 @@ class PackedLoraTrainer:
         # gate/up GEMM with the SwiGLU forward in its epilogue (CTA-pair tiles: ffn shard >= 256)
         self._fuse_swiglu = self.targets[4].h_out >= 256 and fuse_swiglu
         self._fuse_dual = bool(fuse_dual)
+        self._fuse_swiglu_bwd = bool(fuse_swiglu_bwd)
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
@@ -623,11 +627,17 @@ class PackedLoraTrainer:
         self._dy_pass(layer, "down", dh, sv.hs["down"], dh_down)                              # K4 + K3
         d_act = ops.linear_expand(meta, dh, lw["down"], False, bank.shadow_of(layer, "down", "A"), dh_down)  # K6
         del dh
-        act = torch.empty_like(sv.g)
-        dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u, act_out=act)  # in place over g, u
-        del d_act
-        ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))         # K5
-        del act, dh_down
+        if self._fuse_swiglu_bwd and meta.nb == 1:   # SwiGLU bwd + K5 in one pass: act stays on chip
+            dg, du = ops.swiglu_bwd_segred(meta, d_act, sv.g, sv.u, dh_down,
+                                           bank.region_flat(bank.G, layer, "down", "A"), out_g=sv.g, out_u=sv.u)
+            del d_act
+        else:
+            act = torch.empty_like(sv.g)
+            dg, du = ew.swiglu_bwd(d_act, sv.g, sv.u, out_g=sv.g, out_u=sv.u, act_out=act)  # in place over g, u
+            del d_act
+            ops.segred(meta, act, dh_down, bank.region_flat(bank.G, layer, "down", "A"))     # K5
+            del act
+        del dh_down
         x2 = sv.x2 if sv.x2 is not None else self._await(pre2)
         sv.x2 = None
         dx2 = self._group_bwd(layer, ("up", "gate"), x2, (sv.hs["up"], sv.hs["gate"]), (du, dg))

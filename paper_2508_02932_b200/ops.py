@@ -292,6 +292,34 @@ def lora_dual(meta: PackMeta, dy: torch.Tensor, bt_sh: torch.Tensor, hs: torch.T
     return dh_out
 
 
+def swiglu_bwd_segred(meta: PackMeta, d_act: torch.Tensor, g: torch.Tensor, u: torch.Tensor, dh: torch.Tensor,
+                      grad_a: torch.Tensor, out_g: torch.Tensor | None = None,
+                      out_u: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """SwiGLU backward fused with the down projection's dA (K5, reference lorapack.py:226 on
+    act = silu(g) u): returns (dg, du) (may alias g / u) and writes dA_i = act_i^T dH_i into
+    grad_a; act is formed on chip and never stored (plora_swiglu_bwd_segred)."""
+    T, ffn = g.shape
+    _on_current_device(g, "g")
+    for t_, nm in ((d_act, "d_act"), (u, "u")):
+        if t_.shape != g.shape:
+            raise ValueError(f"{nm} must have the shape of g {tuple(g.shape)}")
+    _size(dh, "dh", meta.total_tokens * meta.rpad64)
+    _size(grad_a, "grad_a", ffn * meta.rpad16_total)
+    dg = torch.empty_like(g) if out_g is None else out_g
+    du = torch.empty_like(u) if out_u is None else out_u
+    t = _TIMER.start() if _TIMER else None
+    _lib.check(_lib.lib().plora_swiglu_bwd_segred(
+        _stream(), ctypes.byref(_pack(meta)), ffn, _need(d_act, "d_act"), _need(g, "g"), _need(u, "u"),
+        _need(dh, "dh"), _need(dg, "dg"), _need(du, "du"), _need(grad_a, "grad_a", torch.float32)),
+        "plora_swiglu_bwd_segred")
+    _LAUNCHES[0] += 1
+    if t is not None:
+        tr, R = _lora_work(meta)
+        _TIMER.stop("swiglu_segred", t, flops=2.0 * ffn * tr, nbytes=10.0 * T * ffn + 2.0 * tr + 4.0 * ffn * R,
+                    detail=f"M{ffn}")
+    return dg, du
+
+
 def _ptr_array(ts, name, dtype=torch.bfloat16):
     arr = (ctypes.c_void_p * len(ts))(*[_need(t, f"{name}[{j}]", dtype) for j, t in enumerate(ts)])
     return ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), arr
