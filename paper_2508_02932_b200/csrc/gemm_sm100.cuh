@@ -693,7 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1) plora_segred_lpt_kernel(const __g
 #define PLORA_STORE_EVICT_FIRST 0   // pair-epilogue TMA stores with an L2 evict_first policy (experiment knob)
 #endif
 #ifndef PLORA_PAIR_MAXNREG
-#define PLORA_PAIR_MAXNREG 0     // > 0: register cap of the pair kernel instead of launch_bounds(320, 1) (-> 168)
+#define PLORA_PAIR_MAXNREG 0     // > 0: __maxnreg__ instead of launch_bounds(320, 1) (= 168 regs); 184 / 192 / 200
+                                 // compile with fewer SwiGLU-epilogue spills but fail to launch ("too many resources")
 #endif
 #if PLORA_PAIR_MAXNREG > 0
 #define PLORA_PAIR_BOUNDS __maxnreg__(PLORA_PAIR_MAXNREG)
