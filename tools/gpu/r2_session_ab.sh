@@ -1,0 +1,18 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2ab_pytest.log 2>&1; echo pytest_rc=$?
+tail -2 gpurun_out/r2ab_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r2ab_bench.json 2> gpurun_out/r2ab_bench.err; echo bench_rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/r2ab_bench.json').read().strip().splitlines()[-1])
+print({k: d[k] for k in ('value','ms_per_step','gpu_launches')}, d['e2e']['value'], d['roofline']['frac'], d['clocks'], d.get('cpu_baseline',{}).get('value'), d.get('dropin_api',{}).get('value'))
+"
+PLORA_PROFILE_RANGE=1 PLORA_RECORDS_OUT=gpurun_out/r2ab_records.json timeout 1500 ncu --profile-from-start off --clock-control none \
+  --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  --log-file gpurun_out/r2ab_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r2ab_ncu_bench.log 2>&1; echo ncu_rc=$?
+python tools/dram_by_shape.py gpurun_out/r2ab_launches.csv gpurun_out/r2ab_records.json gpurun_out/r2ab_dram_by_shape.json gpurun_out/r2ab_gemm_traffic.json | head -20
+python tools/summarize_launches.py gpurun_out/r2ab_launches.csv gpurun_out/r2ab_launch_summary.json > /dev/null
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:"swiglu_segred" -s 2 -c 1 \
+     -o gpurun_out/ncu_swiglu_segred python tools/dbg/swiglu_one.py > /dev/null 2>&1; echo ncu2_rc=$?
+timeout 1500 python tools/split_projection.py --gpus 1,2,4,8 --steps 5 --warmup 2 --graph > gpurun_out/r2ab_split.log 2>&1; echo split_rc=$?
+grep -v '"projection"' gpurun_out/r2ab_split.log | tail -4
