@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PLORA_ABI_VERSION 8
+#define PLORA_ABI_VERSION 9
 
 /* Device-resident description of one pack (segment index + adapter table).
  * Built by plora_meta_build on the host, copied to device by the caller. */
@@ -144,19 +144,21 @@ PLORA_API int plora_lora_segred(void* stream, const plora_pack_t* pack, int64_t 
 PLORA_API int plora_swiglu_bwd_segred(void* stream, const plora_pack_t* pack, int64_t ffn, const void* d_act,
                     const void* g, const void* u, const void* dH, void* dg, void* du, float* gradA);
 
-/* K4 + K3 in ONE pass over dY (reference lorapack.py:224-225, Cases 2 and 1):
- *   dH[T][64]      = alpha_i * dY_i B_i^T           (bf16, as plora_lora_shrink with L = Bt_sh)
- *   gradB region   = dB_i^T = Hs_i^T dY_i per segment (f32, as plora_lora_segred; may be NULL)
- * dY bf16 [T][k], Bt_sh bf16 [n][k][64], Hs bf16 [T][64].  Every dY tile is read once and
- * feeds both tensor-core contractions; cross-tile sums go through fp32 partials in the
- * caller-owned workspace ws (plora_lora_dual_workspace_bytes; no zero-fill needed) and a
- * deterministic fix-up.  h_rpad_off = HOST copy of the rpad16 prefix sums [n+1]; the pack
- * must carry h_row_off.  Packs that do not fill the SMs (or nb > 1, k % 128 != 0, or a
- * workspace smaller than required) run the separate K4 / K3 kernels instead. */
-PLORA_API int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off);
-PLORA_API int plora_lora_dual(void* stream, const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off,
-                    const void* dY, const void* Bt_sh, const void* Hs, void* dH, float* gradB,
-                    void* ws, int64_t ws_bytes);
+/* K4 + K3 in ONE pass over dY (reference lorapack.py:224-225, Cases 2 and 1), for 1..3
+ * targets of the pack in one launch (q/k/v or gate/up of a layer):
+ *   dH[t][T][64]   = alpha_i * dY[t]_i B[t]_i^T       (bf16, as plora_lora_shrink with L = Bt_sh[t])
+ *   gradB[t]       = dB_i^T = Hs[t]_i^T dY[t]_i        (f32 region, as plora_lora_segred; may be NULL)
+ * dY[t] bf16 [T][ks[t]], Bt_sh[t] bf16 [n][ks[t]][64], Hs[t] bf16 [T][64].  Every dY tile is
+ * read once and feeds both tensor-core contractions; cross-tile sums go through fp32 partials
+ * in the caller-owned workspace ws (plora_lora_dual_workspace_bytes; no zero-fill needed) and a
+ * deterministic fix-up.  h_rpad_off = HOST copy of the rpad16 prefix sums [n+1]; the pack must
+ * carry h_row_off.  Packs whose targets a time model expects to run faster as separate
+ * passes (or nb > 1, k % 128 != 0, too small a workspace) run the separate K4 / K3 kernels. */
+PLORA_API int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int32_t n_targets, const int64_t* ks,
+                    const int32_t* h_rpad_off);
+PLORA_API int plora_lora_dual(void* stream, const plora_pack_t* pack, int32_t n_targets, const int64_t* ks,
+                    const int32_t* h_rpad_off, const void* const* dY, const void* const* Bt_sh,
+                    const void* const* Hs, void* const* dH, float* const* gradB, void* ws, int64_t ws_bytes);
 
 /* Multi-target K2a / K5 for n_multi (1..3) targets that share their input P (the
  * normed layer input of q/k/v, or of gate/up): P is read ONCE for all targets.

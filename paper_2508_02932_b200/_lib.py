@@ -59,7 +59,7 @@ EXPORTS = (
     "plora_tp_broadcast",
 )
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 
 class PloraError(RuntimeError):
@@ -116,8 +116,9 @@ _SIGNATURES = {
                                  ctypes.POINTER(_vp)], ctypes.c_int),
     "plora_lora_segred_multi": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _i32, ctypes.POINTER(_vp),
                                  ctypes.POINTER(_vp)], ctypes.c_int),
-    "plora_lora_dual_workspace_bytes": ([ctypes.POINTER(PackStruct), _i64, _p32], _i64),
-    "plora_lora_dual": ([_vp, ctypes.POINTER(PackStruct), _i64, _p32, _vp, _vp, _vp, _vp, _vp, _vp, _i64],
+    "plora_lora_dual_workspace_bytes": ([ctypes.POINTER(PackStruct), _i32, _p64, _p32], _i64),
+    "plora_lora_dual": ([_vp, ctypes.POINTER(PackStruct), _i32, _p64, _p32, ctypes.POINTER(_vp),
+                         ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _i64],
                         ctypes.c_int),
     "plora_swiglu_bwd_segred": ([_vp, ctypes.POINTER(PackStruct), _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
                                 ctypes.c_int),

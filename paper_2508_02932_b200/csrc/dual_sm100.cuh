@@ -36,43 +36,52 @@ namespace plora {
 
 constexpr int kDualRC = 4;                 // m-tiles per unit
 constexpr int kDualStages = 4;             // dY ring: [128 rows][128 cols] bf16 = 32 KB per stage
-constexpr int kDualMaxUnits = 3072;
-constexpr int kDualMaxAdapters = 512;
+constexpr int kDualMaxUnits = 2560;
+constexpr int kDualMaxAdapters = 256;
+constexpr int kDualMaxTargets = 3;         // targets of one launch (q/k/v or gate/up share the pack)
 constexpr int kDualYBytes = 32768;
 constexpr int kDualLBytes = 16384;         // L_i slice [128 k][64 r]
 constexpr int kDualHBytes = 16384;         // Hs tile [128 tokens][64 r]
 constexpr int kDualSmemBytes = kDualStages * kDualYBytes + 2 * kDualLBytes + kDualRC * kDualHBytes +
                                1024 /*align*/ + 256 /*barriers*/;
 
-// Host-built unit list (kernel parameter space).  unit[u] = g0 | (rc - 1) << 20 | c << 22:
-// first m-tile index g0 in the pack's 128-row tile list, rc consecutive m-tiles of one
-// adapter, column chunk c.  boff[u] = float offset / 16 of the unit's dB partial block.
+// Host-built unit list (kernel parameter space).  unit[u] = g0 | (rc - 1) << 20 | c << 22 |
+// target << 25: first m-tile index g0 in the pack's 128-row tile list, rc consecutive m-tiles
+// of one adapter, column chunk c (< 8) of target `target` (one launch serves up to 3 targets
+// of a layer that share the pack).  boff[u] = float offset / 16 of the unit's dB partials.
+struct DualTarget {
+  int32_t k;         // dY width (h_out of the target)
+  int32_t kc;        // column-chunk width (multiple of 128)
+  int32_t nc;        // column chunks
+  int32_t pad;
+};
 struct DualSched {
   int32_t n_units;
-  int32_t nc;        // column chunks
-  int32_t kc;        // chunk width (multiple of 128)
-  int32_t k;
+  int32_t n_targets;
+  int32_t pad[2];
+  DualTarget tg[kDualMaxTargets];
   uint32_t unit[kDualMaxUnits];
   uint32_t boff[kDualMaxUnits];
 };
 
 struct __align__(64) DualArgs {
-  CUtensorMap tmY;   // dY [T][k], box {64 cols, 128 rows}
-  CUtensorMap tmL;   // Bt_sh [n][k][64], box {64, 64, 1}
-  CUtensorMap tmH;   // Hs [T][64], box {64, 128 rows}
+  CUtensorMap tmY[kDualMaxTargets];   // dY [T][k], box {64 cols, 128 rows}
+  CUtensorMap tmL[kDualMaxTargets];   // Bt_sh [n][k][64], box {64, 64, 1}
+  CUtensorMap tmH[kDualMaxTargets];   // Hs [T][64], box {64, 128 rows}
   const int32_t* mtiles;    // [n_mtiles][4] {m0, m_len, adapter, 0}
   const float* alpha;
   const int32_t* rpad_off;
-  __nv_bfloat16* dH;        // [T][64] bf16 (written directly when nc == 1)
-  float* part_b;            // dB partials
-  float* part_h;            // [nc][T][64] fp32 dH partials (nc > 1)
+  __nv_bfloat16* dH[kDualMaxTargets];   // [T][64] bf16 (written directly when nc == 1)
+  float* part_b;                        // dB partials (all targets)
+  float* part_h[kDualMaxTargets];       // [nc][T][64] fp32 dH partials (nc > 1)
   int64_t T;
 };
 
-__device__ __forceinline__ void dual_decode(uint32_t u, int& g0, int& rc, int& c) {
+__device__ __forceinline__ void dual_decode(uint32_t u, int& g0, int& rc, int& c, int& tg) {
   g0 = static_cast<int>(u & 0xFFFFFu);
   rc = static_cast<int>((u >> 20) & 3u) + 1;
-  c = static_cast<int>(u >> 22);
+  c = static_cast<int>((u >> 22) & 7u);
+  tg = static_cast<int>(u >> 25);
 }
 
 __global__ void __launch_bounds__(192, 1)
@@ -96,13 +105,12 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int kc = sched.kc;
-  const int k = sched.k;
-
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&args.tmY);
-    tma_prefetch(&args.tmL);
-    tma_prefetch(&args.tmH);
+    for (int t = 0; t < sched.n_targets; ++t) {
+      tma_prefetch(&args.tmY[t]);
+      tma_prefetch(&args.tmL[t]);
+      tma_prefetch(&args.tmH[t]);
+    }
     for (int s = 0; s < kDualStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -133,8 +141,9 @@ __global__ void __launch_bounds__(192, 1)
       int st = 0, ls = 0;
       uint32_t ph = 0, lph = 0, hph = 0;
       for (int ui = blockIdx.x; ui < sched.n_units; ui += gridDim.x) {
-        int g0, rc, c;
-        dual_decode(sched.unit[ui], g0, rc, c);
+        int g0, rc, c, tg;
+        dual_decode(sched.unit[ui], g0, rc, c, tg);
+        const int k = sched.tg[tg].k, kc = sched.tg[tg].kc;
         const int4* mt = reinterpret_cast<const int4*>(args.mtiles) + g0;
         const int a = mt[0].z;
         const int col0 = c * kc;
@@ -143,15 +152,15 @@ __global__ void __launch_bounds__(192, 1)
           const int kcol = col0 + s * 128;
           mbar_wait(&lempty[ls], lph ^ 1);
           mbar_expect_tx(&lfull[ls], kDualLBytes);
-          tma_load_3d(sL + ls * kDualLBytes, &args.tmL, &lfull[ls], 0, kcol, a);
-          tma_load_3d(sL + ls * kDualLBytes + 8192, &args.tmL, &lfull[ls], 0, kcol + 64, a);
+          tma_load_3d(sL + ls * kDualLBytes, &args.tmL[tg], &lfull[ls], 0, kcol, a);
+          tma_load_3d(sL + ls * kDualLBytes + 8192, &args.tmL[tg], &lfull[ls], 0, kcol + 64, a);
           if (++ls == 2) { ls = 0; lph ^= 1; }
           for (int j = 0; j < rc; ++j) {
             const int m0 = mt[j].x;
             mbar_wait(&empty[st], ph ^ 1);
             mbar_expect_tx(&full[st], kDualYBytes);
-            tma_load_2d(sY + st * kDualYBytes, &args.tmY, &full[st], kcol, m0);
-            tma_load_2d(sY + st * kDualYBytes + 16384, &args.tmY, &full[st], kcol + 64, m0);
+            tma_load_2d(sY + st * kDualYBytes, &args.tmY[tg], &full[st], kcol, m0);
+            tma_load_2d(sY + st * kDualYBytes + 16384, &args.tmY[tg], &full[st], kcol + 64, m0);
             if (++st == kDualStages) { st = 0; ph ^= 1; }
           }
           if (s == 0) {
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(hempty, hph ^ 1);
             hph ^= 1;
             mbar_expect_tx(hfull, rc * kDualHBytes);
-            for (int j = 0; j < rc; ++j) tma_load_2d(sH + j * kDualHBytes, &args.tmH, hfull, 0, mt[j].x);
+            for (int j = 0; j < rc; ++j) tma_load_2d(sH + j * kDualHBytes, &args.tmH[tg], hfull, 0, mt[j].x);
           }
         }
       }
@@ -170,8 +179,9 @@ __global__ void __launch_bounds__(192, 1)
     int st = 0, ls = 0, bb = 0;
     uint32_t ph = 0, lph = 0, hph = 0, bph = 0, dph = 0;
     for (int ui = blockIdx.x; ui < sched.n_units; ui += gridDim.x) {
-      int g0, rc, c;
-      dual_decode(sched.unit[ui], g0, rc, c);
+      int g0, rc, c, tg;
+      dual_decode(sched.unit[ui], g0, rc, c, tg);
+      const int k = sched.tg[tg].k, kc = sched.tg[tg].kc;
       const int4* mt = reinterpret_cast<const int4*>(args.mtiles) + g0;
       const int col0 = c * kc;
       const int nsteps = (min(kc, k - col0)) / 128;
@@ -257,8 +267,9 @@ __global__ void __launch_bounds__(192, 1)
     int bb = 0;
     uint32_t bph = 0, dph = 0;
     for (int ui = blockIdx.x; ui < sched.n_units; ui += gridDim.x) {
-      int g0, rc, c;
-      dual_decode(sched.unit[ui], g0, rc, c);
+      int g0, rc, c, tg;
+      dual_decode(sched.unit[ui], g0, rc, c, tg);
+      const int k = sched.tg[tg].k, kc = sched.tg[tg].kc, nc = sched.tg[tg].nc;
       const int4* mt = reinterpret_cast<const int4*>(args.mtiles) + g0;
       const int a = mt[0].z;
       const int rp = args.rpad_off[a + 1] - args.rpad_off[a];   // rpad16 of this adapter (<= 64)
@@ -310,8 +321,8 @@ __global__ void __launch_bounds__(192, 1)
             for (int q = 0; q < 32; ++q) r[q] = 0u;
           }
           if (!ok) continue;
-          if (sched.nc == 1) {   // complete: alpha-scaled bf16 dH (zero past the rank: L is zero-padded)
-            __nv_bfloat16* o = args.dH + t * 64 + h * 32;
+          if (nc == 1) {   // complete: alpha-scaled bf16 dH (zero past the rank: L is zero-padded)
+            __nv_bfloat16* o = args.dH[tg] + t * 64 + h * 32;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 w;
@@ -322,7 +333,7 @@ __global__ void __launch_bounds__(192, 1)
               reinterpret_cast<uint4*>(o)[q] = w;
             }
           } else if (h * 32 < rp) {
-            float* o = args.part_h + (static_cast<int64_t>(c) * args.T + t) * 64 + h * 32;
+            float* o = args.part_h[tg] + (static_cast<int64_t>(c) * args.T + t) * 64 + h * 32;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               if (h * 32 + q * 4 < rp)
@@ -346,30 +357,40 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-// Fix-up of the fused pass (deterministic: fixed summation order).
-//   blocks [0, nb_b): grad region of dB^T, one float4 per thread:
-//     G[k rpad_off[a] + kr rp_a + col] = sum_{q < nq_a} Pb[unit(a, q, kr / kc)][kr % kc][col]
-//   blocks [nb_b, ...) (nc > 1): one per m-tile, dH[t][:] = bf16(alpha_a sum_c Ph[c][t][:]).
+// Fix-up of the fused pass (deterministic: fixed summation order), every target of the
+// launch in one grid:
+//   blocks [bB[t], bB[t+1]): the dB^T grad region of target t, one float4 per thread:
+//     G_t[k rpad_off[a] + kr rp_a + col] = sum_{q < nq_a} Pb[unit(t, a, q, kr / kc)][kr % kc][col]
+//   blocks [bH[t], bH[t+1]) (nc_t > 1): one per m-tile, dH_t[t][:] = bf16(alpha_a sum_c Ph_t[c][t][:]).
 struct DualFix {
   int32_t n;          // adapters
-  int32_t nc, kc, k;
-  int32_t nb_b;       // dB blocks
-  int32_t ubase[kDualMaxAdapters + 1];   // first unit of adapter a (units ordered a, q, c)
+  int32_t n_targets;
+  int32_t bB[kDualMaxTargets + 1];
+  int32_t bH[kDualMaxTargets + 1];
+  int32_t ubase[kDualMaxTargets][kDualMaxAdapters + 1];   // first unit of (target, adapter): units ordered t, a, q, c
+};
+struct DualOut {
+  float* G[kDualMaxTargets];
+  __nv_bfloat16* dH[kDualMaxTargets];
+  const float* part_h[kDualMaxTargets];
 };
 
 __global__ void __launch_bounds__(256) plora_dual_fix_kernel(const __grid_constant__ DualFix f,
                                                              const __grid_constant__ DualSched sched,
+                                                             const __grid_constant__ DualOut out,
                                                              const float* __restrict__ part_b,
-                                                             const float* __restrict__ part_h,
                                                              const int32_t* __restrict__ rpad_off,
                                                              const float* __restrict__ alpha,
-                                                             const int32_t* __restrict__ mtiles, int64_t T,
-                                                             float* __restrict__ G, __nv_bfloat16* __restrict__ dH) {
+                                                             const int32_t* __restrict__ mtiles, int64_t T) {
   pdl_wait();
   pdl_trigger();
-  if (static_cast<int>(blockIdx.x) < f.nb_b) {
-    const int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;   // element of G
-    const int64_t k = f.k;
+  const int b = static_cast<int>(blockIdx.x);
+  if (b < f.bB[f.n_targets]) {
+    int tg = 0;
+    while (b >= f.bB[tg + 1]) ++tg;
+    const DualTarget& tt = sched.tg[tg];
+    const int64_t e = (static_cast<int64_t>(b - f.bB[tg]) * blockDim.x + threadIdx.x) * 4;   // element of G_t
+    const int64_t k = tt.k;
     if (e >= k * rpad_off[f.n]) return;
     int lo = 0, hi = f.n - 1;   // adapter a: k * rpad_off[a] <= e < k * rpad_off[a + 1]
     while (lo < hi) {
@@ -382,12 +403,13 @@ __global__ void __launch_bounds__(256) plora_dual_fix_kernel(const __grid_consta
     const int64_t o = e - k * rpad_off[a];
     const int kr = static_cast<int>(o / rp);
     const int col = static_cast<int>(o - static_cast<int64_t>(kr) * rp);
-    const int c = kr / f.kc;
-    const int kk = kr - c * f.kc;
-    const int nq = (f.ubase[a + 1] - f.ubase[a]) / f.nc;
+    const int c = kr / tt.kc;
+    const int kk = kr - c * tt.kc;
+    const int u0 = f.ubase[tg][a];
+    const int nq = (f.ubase[tg][a + 1] - u0) / tt.nc;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int q = 0; q < nq; ++q) {
-      const int u = f.ubase[a] + q * f.nc + c;
+      const int u = u0 + q * tt.nc + c;
       const float4 v = __ldcs(reinterpret_cast<const float4*>(part_b + static_cast<size_t>(sched.boff[u]) * 16 +
                                                               static_cast<int64_t>(kk) * rp + col));
       acc.x += v.x;
@@ -395,14 +417,19 @@ __global__ void __launch_bounds__(256) plora_dual_fix_kernel(const __grid_consta
       acc.z += v.z;
       acc.w += v.w;
     }
-    *reinterpret_cast<float4*>(G + e) = acc;
+    *reinterpret_cast<float4*>(out.G[tg] + e) = acc;
     return;
   }
-  // dH: one block per 128-row m-tile; thread -> (row, 8 columns)
-  const int4 m = reinterpret_cast<const int4*>(mtiles)[blockIdx.x - f.nb_b];
+  // dH: one block per (target, 128-row m-tile); thread -> (row, 8 columns)
+  int tg = 0;
+  while (b >= f.bH[tg + 1]) ++tg;
+  const int nc = sched.tg[tg].nc;
+  const int4 m = reinterpret_cast<const int4*>(mtiles)[b - f.bH[tg]];
   const int a = m.z;
   const int rp = rpad_off[a + 1] - rpad_off[a];
   const float al = alpha[a];
+  const float* ph = out.part_h[tg];
+  __nv_bfloat16* dH = out.dH[tg];
   for (int i = threadIdx.x; i < m.y * 8; i += blockDim.x) {
     const int r = i >> 3, c8 = (i & 7) * 8;
     const int64_t t = static_cast<int64_t>(m.x) + r;
@@ -410,8 +437,8 @@ __global__ void __launch_bounds__(256) plora_dual_fix_kernel(const __grid_consta
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = 0.f;
     if (c8 < rp) {
-      for (int c = 0; c < f.nc; ++c) {
-        const float4* p = reinterpret_cast<const float4*>(part_h + (static_cast<int64_t>(c) * T + t) * 64 + c8);
+      for (int c = 0; c < nc; ++c) {
+        const float4* p = reinterpret_cast<const float4*>(ph + (static_cast<int64_t>(c) * T + t) * 64 + c8);
         const float4 x = __ldcs(p), y = __ldcs(p + 1);
         v[0] += x.x; v[1] += x.y; v[2] += x.z; v[3] += x.w;
         v[4] += y.x; v[5] += y.y; v[6] += y.z; v[7] += y.w;

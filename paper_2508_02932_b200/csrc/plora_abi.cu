@@ -738,29 +738,27 @@ struct DualPlan {
   DualSched sched;
   DualFix fix;
   int64_t part_b_floats;
+  int64_t part_h_off[kDualMaxTargets];   // float offsets (after the dB partials) of each target's dH partials
   int64_t part_h_floats;
 };
 
-static int64_t dual_plan(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, DualPlan* plan) {
+// Best (rows per chunk, column chunks) of one target by the time model; 0 = the separate
+// kernels are expected to be faster.
+static void dual_choose(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, int* rcs_out, int* nc_out) {
+  *rcs_out = 0;
+  *nc_out = 0;
   const int n = pack->n_adapters;
-  if (!pack->h_row_off || !h_rpad_off || pack->nb != 1 || k <= 0 || k % 128 || n > kDualMaxAdapters ||
-      k > (1 << 24))
-    return -1;
   const int sms = num_sms();
   const int64_t T = pack->total_tokens;
   int64_t sum_rp = 0, tiles_all = 0;
   for (int a = 0; a < n; ++a) {
-    const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
-    if (rp <= 0 || rp > 64) return -1;
     const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
-    sum_rp += rp * tiles;   // sum over m-tiles of rpad16 (partials scale with it)
+    sum_rp += (h_rpad_off[a + 1] - h_rpad_off[a]) * tiles;   // partials scale with rpad16 per m-tile
     tiles_all += tiles;
   }
-  if (tiles_all == 0) return -1;
+  if (tiles_all == 0) return;
   const double avg_rp = static_cast<double>(sum_rp) / tiles_all;
-  const double sep_us = 2.0 * PLORA_DUAL_LAUNCH_US + 4.0 * T * k / (PLORA_DUAL_HBM_GBS * 1e3);
-  double best_us = sep_us;
-  int best_rcs = 0, best_nc = 0;
+  double best_us = 2.0 * PLORA_DUAL_LAUNCH_US + 4.0 * T * k / (PLORA_DUAL_HBM_GBS * 1e3);   // separate K4 + K3
   for (int rcs : {4, 2, 1}) {
     int64_t chunks = 0;
     for (int a = 0; a < n; ++a) {
@@ -777,80 +775,126 @@ static int64_t dual_plan(const plora_pack_t* pack, int64_t k, const int32_t* h_r
       const double us = waves * unit_us + 2.0 * part_bytes / (PLORA_DUAL_HBM_GBS * 1e3) + PLORA_DUAL_LAUNCH_US;
       if (us < best_us) {
         best_us = us;
-        best_rcs = rcs;
-        best_nc = nc;
+        *rcs_out = rcs;
+        *nc_out = nc;
       }
     }
   }
-  if (best_rcs == 0) return -1;
-  const int rcs = best_rcs;
-  int nc = best_nc;
-  const int kc = static_cast<int>(((k + nc - 1) / nc + 127) / 128 * 128);
-  nc = static_cast<int>((k + kc - 1) / kc);
-  DualSched& sc = plan->sched;
-  DualFix& f = plan->fix;
-  sc.nc = f.nc = nc;
-  sc.kc = f.kc = kc;
-  sc.k = f.k = static_cast<int>(k);
-  f.n = n;
-  int u = 0;
-  int64_t g = 0, boff = 0;   // boff in floats
+}
+
+// Plan of one fused launch over n_t targets of the pack (dY widths ks[t]) -- every target
+// gets its own (rows per chunk, column chunks) from dual_choose; the units of all targets
+// go into one unit list.  Returns the workspace bytes, or -1 when a target would be faster
+// with the separate kernels or the pack is not eligible (rank blocks > 1, k % 128 != 0,
+// unit list or adapter table too large): then every target runs separately.
+static int64_t dual_plan(const plora_pack_t* pack, int n_t, const int64_t* ks, const int32_t* h_rpad_off,
+                         DualPlan* plan) {
+  const int n = pack->n_adapters;
+  if (!pack->h_row_off || !h_rpad_off || pack->nb != 1 || n > kDualMaxAdapters || n_t < 1 || n_t > kDualMaxTargets)
+    return -1;
   for (int a = 0; a < n; ++a) {
-    f.ubase[a] = u;
-    const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
     const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
     if (rp <= 0 || rp > 64) return -1;
-    for (int64_t q = 0; q < tiles; q += rcs) {
-      const int rc = static_cast<int>(tiles - q < rcs ? tiles - q : rcs);
-      if (g + q >= (1 << 20)) return -1;
-      for (int c = 0; c < nc; ++c) {
-        sc.unit[u] = static_cast<uint32_t>(g + q) | static_cast<uint32_t>(rc - 1) << 20 | static_cast<uint32_t>(c) << 22;
-        sc.boff[u] = static_cast<uint32_t>(boff / 16);
-        boff += static_cast<int64_t>(kc) * rp;   // a multiple of 16 floats
-        ++u;
-      }
-    }
-    g += tiles;
   }
-  f.ubase[n] = u;
+  DualSched& sc = plan->sched;
+  DualFix& f = plan->fix;
+  sc.n_targets = f.n_targets = n_t;
+  f.n = n;
+  int u = 0;
+  int64_t boff = 0;   // floats
+  int rcs_t[kDualMaxTargets];
+  for (int t = 0; t < n_t; ++t) {
+    const int64_t k = ks[t];
+    if (k <= 0 || k % 128 || k > (1 << 24)) return -1;
+    int rcs, nc;
+    dual_choose(pack, k, h_rpad_off, &rcs, &nc);
+    if (rcs == 0) return -1;
+    const int kc = static_cast<int>(((k + nc - 1) / nc + 127) / 128 * 128);
+    nc = static_cast<int>((k + kc - 1) / kc);
+    sc.tg[t].k = static_cast<int>(k);
+    sc.tg[t].kc = kc;
+    sc.tg[t].nc = nc;
+    rcs_t[t] = rcs;
+  }
+  for (int t = 0; t < n_t; ++t) {
+    const int rcs = rcs_t[t], nc = sc.tg[t].nc, kc = sc.tg[t].kc;
+    int64_t g = 0;
+    for (int a = 0; a < n; ++a) {
+      f.ubase[t][a] = u;
+      const int64_t tiles = (pack->h_row_off[a + 1] - pack->h_row_off[a] + kBM - 1) / kBM;
+      const int rp = h_rpad_off[a + 1] - h_rpad_off[a];
+      for (int64_t q = 0; q < tiles; q += rcs) {
+        const int rc = static_cast<int>(tiles - q < rcs ? tiles - q : rcs);
+        if (g + q >= (1 << 20) || u + nc > kDualMaxUnits) return -1;
+        for (int c = 0; c < nc; ++c) {
+          sc.unit[u] = static_cast<uint32_t>(g + q) | static_cast<uint32_t>(rc - 1) << 20 |
+                       static_cast<uint32_t>(c) << 22 | static_cast<uint32_t>(t) << 25;
+          sc.boff[u] = static_cast<uint32_t>(boff / 16);
+          boff += static_cast<int64_t>(kc) * rp;   // a multiple of 16 floats
+          ++u;
+        }
+      }
+      g += tiles;
+    }
+    f.ubase[t][n] = u;
+  }
   sc.n_units = u;
   plan->part_b_floats = boff;
-  plan->part_h_floats = nc > 1 ? static_cast<int64_t>(nc) * pack->total_tokens * 64 : 0;
+  int64_t ph = 0;
+  for (int t = 0; t < n_t; ++t) {
+    plan->part_h_off[t] = boff + ph;
+    if (sc.tg[t].nc > 1) ph += static_cast<int64_t>(sc.tg[t].nc) * pack->total_tokens * 64;
+  }
+  plan->part_h_floats = ph;
   return (plan->part_b_floats + plan->part_h_floats) * 4 + 256;
 }
 
-static int run_dual(cudaStream_t st, const plora_pack_t* pack, int64_t k, const DualPlan& plan, const void* dY,
-                    const void* Bt_sh, const void* Hs, void* dH, float* gradB, void* ws) {
+static int run_dual(cudaStream_t st, const plora_pack_t* pack, const DualPlan& plan, const void* const* dY,
+                    const void* const* Bt_sh, const void* const* Hs, void* const* dH, float* const* gradB, void* ws) {
   const int64_t T = pack->total_tokens;
-  DualArgs a;
-  memset(&a, 0, sizeof(a));
+  const int n_t = plan.sched.n_targets;
+  auto a = std::make_unique<DualArgs>();
+  memset(a.get(), 0, sizeof(DualArgs));
+  DualOut out;
+  memset(&out, 0, sizeof(out));
   int rc;
-  if ((rc = make_map_2d(&a.tmY, dY, k, T, k, 64, kBM))) return rc;
-  if ((rc = make_map_3d(&a.tmL, Bt_sh, 64, k, pack->n_adapters, 64, 64))) return rc;
-  if ((rc = make_map_2d(&a.tmH, Hs, 64, T, 64, 64, kBM))) return rc;
   float* part_b = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
-  a.mtiles = pack->d_mtiles;
-  a.alpha = pack->d_alpha;
-  a.rpad_off = pack->d_rpad_off;
-  a.dH = static_cast<__nv_bfloat16*>(dH);
-  a.part_b = part_b;
-  a.part_h = part_b + plan.part_b_floats;
-  a.T = T;
+  for (int t = 0; t < n_t; ++t) {
+    const int64_t k = plan.sched.tg[t].k;
+    if ((rc = make_map_2d(&a->tmY[t], dY[t], k, T, k, 64, kBM))) return rc;
+    if ((rc = make_map_3d(&a->tmL[t], Bt_sh[t], 64, k, pack->n_adapters, 64, 64))) return rc;
+    if ((rc = make_map_2d(&a->tmH[t], Hs[t], 64, T, 64, 64, kBM))) return rc;
+    a->dH[t] = static_cast<__nv_bfloat16*>(dH[t]);
+    a->part_h[t] = part_b + plan.part_h_off[t];
+    out.G[t] = gradB[t];
+    out.dH[t] = static_cast<__nv_bfloat16*>(dH[t]);
+    out.part_h[t] = a->part_h[t];
+  }
+  a->mtiles = pack->d_mtiles;
+  a->alpha = pack->d_alpha;
+  a->rpad_off = pack->d_rpad_off;
+  a->part_b = part_b;
+  a->T = T;
   static std::atomic<uint64_t> configured{0};
   if (ensure_smem(plora_dual_kernel, kDualSmemBytes, configured)) return 1;
   const int grid = plan.sched.n_units < num_sms() ? plan.sched.n_units : num_sms();
-  PLORA_CUDA(launch_pdl(plora_dual_kernel, dim3(grid), dim3(192), kDualSmemBytes, st, a, plan.sched));
-  PLORA_CUDA(cudaGetLastError());
-  DualFix f = plan.fix;
-  const int64_t g4 = gradB ? (k * pack->rpad16_total + 3) / 4 : 0;   // float4s of the dB^T region
-  f.nb_b = static_cast<int>((g4 + 255) / 256);
-  const int nb_h = plan.sched.nc > 1 ? pack->n_mtiles : 0;
-  if (f.nb_b + nb_h > 0) {
-    PLORA_CUDA(launch_pdl(plora_dual_fix_kernel, dim3(f.nb_b + nb_h), dim3(256), 0, st, f, plan.sched,
-                          static_cast<const float*>(part_b), static_cast<const float*>(a.part_h),
-                          pack->d_rpad_off, pack->d_alpha, pack->d_mtiles, T, gradB,
-                          static_cast<__nv_bfloat16*>(dH)));
-    PLORA_CUDA(cudaGetLastError());
+  PLORA_CUDA(launch_pdl(plora_dual_kernel, dim3(grid), dim3(192), kDualSmemBytes, st, *a, plan.sched));
+  auto f = std::make_unique<DualFix>(plan.fix);
+  int blocks = 0;
+  for (int t = 0; t < n_t; ++t) {   // dB blocks of every target, then the dH blocks
+    f->bB[t] = blocks;
+    if (gradB[t]) blocks += static_cast<int>(((plan.sched.tg[t].k * pack->rpad16_total + 3) / 4 + 255) / 256);
+  }
+  f->bB[n_t] = blocks;
+  for (int t = n_t + 1; t <= kDualMaxTargets; ++t) f->bB[t] = blocks;
+  for (int t = 0; t < n_t; ++t) {
+    f->bH[t] = blocks;
+    if (plan.sched.tg[t].nc > 1) blocks += pack->n_mtiles;
+  }
+  for (int t = n_t; t <= kDualMaxTargets; ++t) f->bH[t] = blocks;
+  if (blocks > 0) {
+    PLORA_CUDA(launch_pdl(plora_dual_fix_kernel, dim3(blocks), dim3(256), 0, st, *f, plan.sched, out,
+                          static_cast<const float*>(part_b), pack->d_rpad_off, pack->d_alpha, pack->d_mtiles, T));
   }
   return 0;
 }
@@ -941,28 +985,36 @@ int plora_swiglu_bwd_segred(void* stream, const plora_pack_t* pack, int64_t ffn,
   return run_swiglu_segred(static_cast<cudaStream_t>(stream), pack, ffn, d_act, g, u, dH, dg, du, gradA);
 }
 
-int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off) {
-  if (check_pack(pack)) return -1;
+int64_t plora_lora_dual_workspace_bytes(const plora_pack_t* pack, int32_t n_targets, const int64_t* ks,
+                                        const int32_t* h_rpad_off) {
+  if (check_pack(pack) || !ks) return -1;
   auto plan = std::make_unique<DualPlan>();
-  const int64_t b = dual_plan(pack, k, h_rpad_off, plan.get());
+  const int64_t b = dual_plan(pack, n_targets, ks, h_rpad_off, plan.get());
   return b < 0 ? 0 : b;
 }
 
-int plora_lora_dual(void* stream, const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, const void* dY,
-                    const void* Bt_sh, const void* Hs, void* dH, float* gradB, void* ws, int64_t ws_bytes) {
+int plora_lora_dual(void* stream, const plora_pack_t* pack, int32_t n_targets, const int64_t* ks,
+                    const int32_t* h_rpad_off, const void* const* dY, const void* const* Bt_sh, const void* const* Hs,
+                    void* const* dH, float* const* gradB, void* ws, int64_t ws_bytes) {
   int rc;
   if ((rc = check_pack(pack))) return rc;
-  if (!dY || !Bt_sh || !dH || (gradB && !Hs)) return fail("lora_dual: NULL operand");
+  if (n_targets < 1 || n_targets > kDualMaxTargets) return fail("lora_dual: 1..3 targets");
+  if (!ks || !dY || !Bt_sh || !Hs || !dH || !gradB) return fail("lora_dual: NULL operand array");
+  for (int t = 0; t < n_targets; ++t)
+    if (!dY[t] || !Bt_sh[t] || !dH[t] || (gradB[t] && !Hs[t])) return fail("lora_dual: NULL operand");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (pack->total_tokens > 0 && pack->n_mtiles > 0) {
     auto plan = std::make_unique<DualPlan>();
-    const int64_t need = dual_plan(pack, k, h_rpad_off, plan.get());
+    const int64_t need = dual_plan(pack, n_targets, ks, h_rpad_off, plan.get());
     if (need >= 0 && ws != nullptr && ws_bytes >= need)
-      return run_dual(st, pack, k, *plan, dY, Bt_sh, Hs, dH, gradB, ws);
+      return run_dual(st, pack, *plan, dY, Bt_sh, Hs, dH, gradB, ws);
   }
-  // not eligible (or no workspace): the separate K4 / K3 kernels, same results up to fp32 association
-  if ((rc = run_shrink(st, pack, k, dY, Bt_sh, dH))) return rc;
-  if (gradB && (rc = run_segred(st, pack, k, dY, Hs, gradB))) return rc;
+  // not eligible (or no workspace): the separate K4 / K3 kernels per target, same results up
+  // to fp32 association
+  for (int t = 0; t < n_targets; ++t) {
+    if ((rc = run_shrink(st, pack, ks[t], dY[t], Bt_sh[t], dH[t]))) return rc;
+    if (gradB[t] && (rc = run_segred(st, pack, ks[t], dY[t], Hs[t], gradB[t]))) return rc;
+  }
   return 0;
 }
 

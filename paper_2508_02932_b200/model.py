@@ -510,17 +510,20 @@ class PackedLoraTrainer:
         x.record_stream(side)
         return x, parts
 
-    def _dy_pass(self, layer: int, nm: str, dy: torch.Tensor, hs: torch.Tensor, dh: torch.Tensor) -> None:
-        """Cases 2 and 1 of the reference backward (lorapack.py:225, :224) for one target:
-        dH = alpha dY B^T into ``dh`` and dB^T = Hs^T dY into the grad region -- one fused
-        pass over dY (K4 + K3, ops.lora_dual) or the two separate kernels."""
+    def _dy_pass(self, layer: int, names, dys, hss, dhs) -> None:
+        """Cases 2 and 1 of the reference backward (lorapack.py:225, :224) for the targets
+        ``names`` (one, or the q/k/v / gate/up group): dH = alpha dY B^T into ``dhs`` and
+        dB^T = Hs^T dY into the grad regions -- one fused pass over every dY in one launch
+        (K4 + K3, ops.lora_dual) or the two separate kernels per target."""
         bank, meta = self.bank, self.meta
-        bt, g = bank.shadow_of(layer, nm, "B"), bank.region_flat(bank.G, layer, nm, "B")
+        bts = [bank.shadow_of(layer, nm, "B") for nm in names]
+        gs = [bank.region_flat(bank.G, layer, nm, "B") for nm in names]
         if self._fuse_dual and meta.nb == 1:
-            ops.lora_dual(meta, dy, bt, hs, dh, g)
+            ops.lora_dual(meta, list(dys), bts, list(hss), list(dhs), gs)
         else:
-            ops.shrink(meta, dy, bt, dh)        # K4 (Case 2)
-            ops.segred(meta, dy, hs, g)         # K3 (Case 1)
+            for dy, bt, hs, dh, g in zip(dys, bts, hss, dhs, gs):
+                ops.shrink(meta, dy, bt, dh)        # K4 (Case 2)
+                ops.segred(meta, dy, hs, g)         # K3 (Case 1)
 
     def _group_bwd(self, layer: int, names, x: torch.Tensor, hss, dys, need_dx: bool = True):
         """Backward of targets sharing the input x: per target K4 dH and K3 dB; ONE grouped
@@ -529,11 +532,8 @@ class PackedLoraTrainer:
         partial -- both are all-reduced here (dX per token chunk, overlapping the GEMM),
         dH before dA (tp.py)."""
         bank, meta, lw = self.bank, self.meta, self.base.layers[layer]
-        dhs = []
-        for nm, hs, dy in zip(names, hss, dys):
-            dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
-            self._dy_pass(layer, nm, dy, hs, dh)                                           # K4 + K3
-            dhs.append(dh)
+        dhs = [torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device) for _ in names]
+        self._dy_pass(layer, names, dys, hss, dhs)                                          # K4 + K3
         dx = None
         ws, ashs = [lw[nm] for nm in names], [bank.shadow_of(layer, nm, "A") for nm in names]
         if need_dx and self.tp is not None:   # partial dX_s: chunked all-reduce overlapping the GEMM
@@ -624,7 +624,7 @@ class PackedLoraTrainer:
         dh_s = dh
         dh = self._gather(dh_s)   # sequence parallel: the row-parallel output gradient on all T rows
         dh_down = torch.empty((T, meta.rpad64), dtype=bf16, device=self.device)
-        self._dy_pass(layer, "down", dh, sv.hs["down"], dh_down)                              # K4 + K3
+        self._dy_pass(layer, ("down",), (dh,), (sv.hs["down"],), (dh_down,))                 # K4 + K3
         d_act = ops.linear_expand(meta, dh, lw["down"], False, bank.shadow_of(layer, "down", "A"), dh_down)  # K6
         del dh
         if self._fuse_swiglu_bwd and meta.nb == 1:   # SwiGLU bwd + K5 in one pass: act stays on chip

@@ -260,35 +260,54 @@ def _h_rpad(meta: PackMeta):
     return meta._h_rpad_c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
 
-def lora_dual(meta: PackMeta, dy: torch.Tensor, bt_sh: torch.Tensor, hs: torch.Tensor | None,
-              dh_out: torch.Tensor, g: torch.Tensor | None) -> torch.Tensor:
-    """K4 + K3 in one pass over dY (reference lorapack.py:224-225): dh_out = alpha_i dY_i B_i^T
-    (bf16 [T][rpad64]) and, when g is given, the dB_i^T grad region = Hs_i^T dY_i (fp32).
-    Packs too small to fill the SMs run the separate K4 / K3 kernels (plora_lora_dual)."""
-    T, k = dy.shape
-    _on_current_device(dy, "dy")
-    _lora_shapes(meta, k, bt_sh, dh_out, meta.total_tokens)
-    if g is not None:
-        _size(hs, "hs", meta.total_tokens * meta.rpad64)
-        _size(g, "g", k * meta.rpad16_total)
+def lora_dual(meta: PackMeta, dy, bt_sh, hs, dh_out, g):
+    """K4 + K3 in one pass over dY (reference lorapack.py:224-225) for one target or a list of
+    up to 3 targets of the pack (one launch): dh_out[t] = alpha_i dY[t]_i B[t]_i^T (bf16
+    [T][rpad64]) and, where g[t] is given, the dB_i^T grad region = Hs[t]_i^T dY[t]_i (fp32).
+    Packs a time model expects to run faster as separate passes run the separate K4 / K3
+    kernels (plora_lora_dual)."""
+    multi = isinstance(dy, (list, tuple))
+    dys, bts, hss, dhs, gs = ([x] for x in (dy, bt_sh, hs, dh_out, g)) if not multi else \
+        (list(dy), list(bt_sh), list(hs), list(dh_out), list(g))
+    n_t = len(dys)
+    if not 1 <= n_t <= 3 or not all(len(x) == n_t for x in (bts, hss, dhs, gs)):
+        raise ValueError("lora_dual: 1..3 targets with one dy, bt_sh, hs, dh_out, g each")
+    T = dys[0].shape[0]
+    ks = []
+    for dy_t, bt_t, hs_t, dh_t, g_t in zip(dys, bts, hss, dhs, gs):
+        k = dy_t.shape[1]
+        ks.append(k)
+        _on_current_device(dy_t, "dy")
+        _lora_shapes(meta, k, bt_t, dh_t, meta.total_tokens)
+        if g_t is not None:
+            _size(hs_t, "hs", meta.total_tokens * meta.rpad64)
+            _size(g_t, "g", k * meta.rpad16_total)
     s = _pack(meta)
     rp = _h_rpad(meta)
-    need = int(_lib.lib().plora_lora_dual_workspace_bytes(ctypes.byref(s), k, rp))
+    karr = (ctypes.c_int64 * n_t)(*ks)
+    need = int(_lib.lib().plora_lora_dual_workspace_bytes(ctypes.byref(s), n_t, karr, rp))
     ws = _dual_workspace(need) if need > 0 else None
+    yp, _k1 = _ptr_array(dys, "dy")
+    bp, _k2 = _ptr_array(bts, "bt_sh")
+    hp = (ctypes.c_void_p * n_t)(*[_need(h, "hs", allow_none=gt is None) for h, gt in zip(hss, gs)])
+    op, _k3 = _ptr_array(dhs, "dh_out")
+    gp = (ctypes.c_void_p * n_t)(*[_need(gt, "g", torch.float32, allow_none=True) for gt in gs])
     t = _TIMER.start() if _TIMER else None
-    _lib.check(_lib.lib().plora_lora_dual(_stream(), ctypes.byref(s), k, rp, _need(dy, "dy"), _need(bt_sh, "bt_sh"),
-                                          _need(hs, "hs", allow_none=g is None), _need(dh_out, "dh_out"),
-                                          _need(g, "g", torch.float32, allow_none=True),
+    _lib.check(_lib.lib().plora_lora_dual(_stream(), ctypes.byref(s), n_t, karr, rp, yp, bp,
+                                          ctypes.cast(hp, ctypes.POINTER(ctypes.c_void_p)), op,
+                                          ctypes.cast(gp, ctypes.POINTER(ctypes.c_void_p)),
                                           ws.data_ptr() if ws is not None else None, need),
                "plora_lora_dual")
-    _LAUNCHES[0] += 2 if g is not None else 1
+    _LAUNCHES[0] += 2 if need > 0 else sum(1 + (gt is not None) for gt in gs)
     if t is not None:
         tr, R = _lora_work(meta)
+        ksum = float(sum(ks))
         if need > 0:
-            _TIMER.stop("dual", t, flops=4.0 * k * tr, nbytes=2.0 * T * k + 4.0 * tr + 6.0 * k * R, detail=f"K{k}")
+            _TIMER.stop("dual", t, flops=4.0 * ksum * tr, nbytes=2.0 * T * ksum + n_t * 4.0 * tr + 6.0 * ksum * R,
+                        detail="K" + "+".join(str(k) for k in ks))
         else:   # separate K4 + K3 launches: both passes' algorithmic bytes
-            _TIMER.stop("dual", t, flops=4.0 * k * tr, nbytes=4.0 * T * k + 6.0 * tr + 6.0 * k * R,
-                        detail=f"K{k}sep")
+            _TIMER.stop("dual", t, flops=4.0 * ksum * tr, nbytes=4.0 * T * ksum + n_t * 6.0 * tr + 6.0 * ksum * R,
+                        detail="K" + "+".join(str(k) for k in ks) + "sep")
     return dh_out
 
 

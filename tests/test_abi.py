@@ -72,7 +72,8 @@ def test_fused_dy_pass_plan_on_host():
             setattr(s, f, 16)
         h_row = np.ascontiguousarray(meta.row_offsets, dtype=np.int64)
         s.h_row_off = h_row.ctypes.data
-        return int(lib.plora_lora_dual_workspace_bytes(ctypes.byref(s), k, ops._h_rpad(meta))), meta
+        karr = (ctypes.c_int64 * 1)(k)
+        return int(lib.plora_lora_dual_workspace_bytes(ctypes.byref(s), 1, karr, ops._h_rpad(meta))), meta
 
     c3_tokens = [x * 1024 for x in [1, 1, 2, 4, 2, 1, 4, 1, 1, 2, 1, 4, 4, 2, 1, 1]]
     ws, meta = plan([8, 16, 32, 64] * 4, c3_tokens, 4096)

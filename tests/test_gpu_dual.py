@@ -45,8 +45,10 @@ def _operands(ranks, tokens, k, seed):
 
 
 def _fused(meta, k):
+    import ctypes
     s = meta.struct
-    return int(_lib.lib().plora_lora_dual_workspace_bytes(s, k, ops._h_rpad(meta))) > 0
+    karr = (ctypes.c_int64 * 1)(k)
+    return int(_lib.lib().plora_lora_dual_workspace_bytes(ctypes.byref(s), 1, karr, ops._h_rpad(meta))) > 0
 
 
 @pytest.mark.parametrize("name,ranks,tokens,k", CASES)
@@ -127,3 +129,33 @@ def test_trainer_fused_dual_matches_separate():
     # dA inherits the bf16 rounding of dH (a last-bit flip where the fp32 sums associate
     # differently): ~1e-3 relative; dB itself agrees to fp32 association
     assert rel(res[0][1], res[1][1]) < 5e-3
+
+
+@pytest.mark.parametrize("ks", [(4096, 1024, 1024), (14336, 14336)])
+def test_dual_multi_target_one_launch(ks):
+    """The q/k/v (or gate/up) targets of a layer in ONE fused launch equal the separate
+    K4 / K3 kernels per target (fp32 association)."""
+    import ctypes
+    outs, refs = [], []
+    meta = None
+    dys, bts, hss = [], [], []
+    for j, k in enumerate(ks):
+        m, dy, bt, hs = _operands(C3_RANKS, C3_TOKENS, k, seed=20 + j)
+        meta = meta or m
+        dys.append(dy), bts.append(bt), hss.append(hs)
+    T, R64 = meta.total_tokens, meta.rpad64
+    karr = (ctypes.c_int64 * len(ks))(*ks)
+    assert int(_lib.lib().plora_lora_dual_workspace_bytes(ctypes.byref(meta.struct), len(ks), karr,
+                                                          ops._h_rpad(meta))) > 0
+    dhs = [torch.full((T, R64), float("nan"), device="cuda", dtype=bf) for _ in ks]
+    gs = [torch.full((k * meta.rpad16_total,), float("nan"), device="cuda") for k in ks]
+    ops.lora_dual(meta, dys, bts, hss, dhs, gs)
+    for dy, bt, hs, dh, g, k in zip(dys, bts, hss, dhs, gs, ks):
+        dh_sep = torch.empty_like(dh)
+        g_sep = torch.empty_like(g)
+        ops.shrink(meta, dy, bt, dh_sep)
+        ops.segred(meta, dy, hs, g_sep)
+        torch.cuda.synchronize()
+        assert not torch.isnan(dh).any() and not torch.isnan(g).any()
+        assert rel(g, g_sep) < 1e-5, k
+        assert rel(dh, dh_sep) < 2e-3, k

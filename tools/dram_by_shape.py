@@ -40,12 +40,16 @@ def launches(path):
 def main(lpath, rpath, out, traffic_out=None):
     ls = [(n, m) for n, m in launches(lpath) if any(k in n for k in TIMED)]
     recs = json.load(open(rpath))
-    need = sum(PER_RECORD.get(r["kind"], 1) for r in recs)
+    def per(r):   # the fused pass: dual + fix-up; its separate fallback: shrink + segred per target
+        if r["kind"] == "dual" and str(r["detail"]).endswith("sep"):
+            return 2 * (str(r["detail"]).count("+") + 1)
+        return PER_RECORD.get(r["kind"], 1)
+    need = sum(per(r) for r in recs)
     if len(ls) != need:
         raise SystemExit(f"{len(ls)} timed-kernel launches in the ncu list but {need} for the bench records")
     pairs, i = [], 0
     for r in recs:
-        k = PER_RECORD.get(r["kind"], 1)
+        k = per(r)
         grp = ls[i:i + k]
         i += k
         m = {key: sum(g[1].get(key, 0.0) for g in grp) for key in grp[0][1]}
