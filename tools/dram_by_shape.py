@@ -13,7 +13,8 @@ import json
 import sys
 from collections import OrderedDict
 
-TIMED = ("plora_gemm_pair_kernel", "plora_gemm_kernel", "plora_segred_lpt_kernel", "adamw_kernel", "plora_dual")
+TIMED = ("plora_gemm_pair_kernel", "plora_gemm_kernel", "plora_segred_lpt_kernel", "adamw_kernel", "plora_dual",
+         "plora_swiglu_segred")
 # launches per record: the fused K3+K4 pass is the dual kernel + its fix-up (or, for packs
 # too small for it, the separate shrink + segment reduction)
 PER_RECORD = {"dual": 2}

@@ -10,6 +10,8 @@ def classify(name: str) -> str:
     m = re.search(r"plora_gemm_pair_kernel<\(bool\)(\d), \(int\)(\d)>|plora_gemm_pair_kernel<(\w+), (\d)>", name)
     if "plora_gemm_pair_kernel" in name:
         return "gemm_pair (K1/K2b fwd, K6 dX, lm_head)"
+    if "plora_swiglu_segred" in name:
+        return "SwiGLU bwd + dA_down (fused)"
     if "plora_dual" in name:
         return "dual K4+K3 (one dY pass + fix-up)"
     if "plora_segred_lpt_kernel" in name:
