@@ -432,8 +432,18 @@ class PackedLoraTrainer:
         return full
 
     def _lin_bwd(self, layer: int, tname: str, x, w, hs, dy, need_dx=True, dx_residual=None, dx_out=None):
-        bank = self.bank
-        return ops.linear_bwd(self.meta, x, w, True, bank.shadow_of(layer, tname, "A"),
+        """Backward of one packed LoRA linear (reference lorapack.py:202-231): Cases 2 + 1 as
+        the fused dY pass, Case 3 (K5), Case 4 (K6) -- or ops.linear_bwd's four kernels."""
+        bank, meta = self.bank, self.meta
+        if self._fuse_dual and meta.nb == 1:
+            dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
+            self._dy_pass(layer, (tname,), (dy,), (hs,), (dh,))                                  # K4 + K3
+            ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A"))                   # K5
+            if not need_dx:
+                return None
+            return ops.linear_expand(meta, dy, w, False, bank.shadow_of(layer, tname, "A"), dh,    # K6
+                                     y_out=dx_out, residual=dx_residual)
+        return ops.linear_bwd(meta, x, w, True, bank.shadow_of(layer, tname, "A"),
                               bank.shadow_of(layer, tname, "B"), hs, dy,
                               bank.region_flat(bank.G, layer, tname, "A"),
                               bank.region_flat(bank.G, layer, tname, "B"),
