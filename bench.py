@@ -347,6 +347,7 @@ def main() -> None:
                     help="TP all-reduce through torch.distributed (NCCL) or libplora's C-ABI (plora_tp_*, NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fuse-dual", action="store_true", help="separate K4 / K3 kernels (A/B of the fused dY pass)")
+    ap.add_argument("--overlap-k5", action="store_true", help="dA reductions on a side stream (A/B)")
     ap.add_argument("--graph", dest="graph", action="store_true", default=True,
                     help="time the step replayed from one CUDA graph (model.GraphedStep; default)")
     ap.add_argument("--eager", dest="graph", action="store_false", help="time the eager step instead")
@@ -413,7 +414,8 @@ def main() -> None:
     T = 0
     if specs:
         trainer = PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=[100 + i + seed_off for i in mine],
-                                    tp=comm, fuse_dual=not args.no_fuse_dual)
+                                    tp=comm, fuse_dual=not args.no_fuse_dual,
+                                    overlap_k5=args.overlap_k5)
         T = trainer.T
         tokens_host = trainer.synthetic_tokens(seeds=[1000 + i + 100 * seed_off for i in mine]).pin_memory()
         tokens = tokens_host.to("cuda")

@@ -212,7 +212,7 @@ class PackedLoraTrainer:
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
                  save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool = False,
                  tp_chunks: int = 4, fuse_swiglu: bool = True, fuse_dual: bool = True,
-                 fuse_swiglu_bwd: bool = True):
+                 fuse_swiglu_bwd: bool = True, overlap_k5: bool = False):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
@@ -224,7 +224,9 @@ class PackedLoraTrainer:
         gate/up GEMM with the SwiGLU forward in its epilogue; ``fuse_dual``: K4 (dH) and K3
         (dB) of every target in one pass over dY (ops.lora_dual) instead of two;
         ``fuse_swiglu_bwd``: the SwiGLU backward and the down projection's dA in one kernel
-        (ops.swiglu_bwd_segred: the activation never goes to HBM)."""
+        (ops.swiglu_bwd_segred: the activation never goes to HBM); ``overlap_k5``: the dA
+        segment reductions (K5, off the critical path: only the optimizer reads dA) run on a
+        side stream beside the input-gradient GEMMs."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -275,6 +277,9 @@ class PackedLoraTrainer:
         self._fuse_swiglu = self.targets[4].h_out >= 256 and fuse_swiglu
         self._fuse_dual = bool(fuse_dual)
         self._fuse_swiglu_bwd = bool(fuse_swiglu_bwd)
+        self._overlap_k5 = bool(overlap_k5) and self.tp is None
+        self._k5_stream = None
+        self._k5_used = False
         self._row_off_dev = torch.tensor(self.meta.row_offsets, dtype=torch.int64, device=self.device)
 
     # ------------------------------------------------------------------ helpers
@@ -438,7 +443,7 @@ class PackedLoraTrainer:
         if self._fuse_dual and meta.nb == 1:
             dh = torch.empty((self.T, meta.rpad64), dtype=bf16, device=self.device)
             self._dy_pass(layer, (tname,), (dy,), (hs,), (dh,))                                  # K4 + K3
-            ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A"))                   # K5
+            self._k5(lambda: ops.segred(meta, x, dh, bank.region_flat(bank.G, layer, tname, "A")), x, dh)  # K5
             if not need_dx:
                 return None
             return ops.linear_expand(meta, dy, w, False, bank.shadow_of(layer, tname, "A"), dh,    # K6
@@ -520,6 +525,22 @@ class PackedLoraTrainer:
         x.record_stream(side)
         return x, parts
 
+    def _k5(self, fn, *tensors) -> None:
+        """Run the dA reduction ``fn`` (K5) in stream order, or -- with overlap_k5 -- on the
+        side stream after the work issued so far (joined before the optimizer step)."""
+        if not self._overlap_k5:
+            fn()
+            return
+        cur = torch.cuda.current_stream()
+        if self._k5_stream is None:
+            self._k5_stream = torch.cuda.Stream(device=self.device)
+        self._k5_stream.wait_stream(cur)
+        with torch.cuda.stream(self._k5_stream):
+            fn()
+        for t in tensors:
+            t.record_stream(self._k5_stream)
+        self._k5_used = True
+
     def _dy_pass(self, layer: int, names, dys, hss, dhs) -> None:
         """Cases 2 and 1 of the reference backward (lorapack.py:225, :224) for the targets
         ``names`` (one, or the q/k/v / gate/up group): dH = alpha dY B^T into ``dhs`` and
@@ -556,7 +577,8 @@ class PackedLoraTrainer:
             if need_dx:   # K6 (Case 4) for every target in one accumulator
                 dx = ops.linear_dx_group(meta, list(dys), ws, ashs, dhs, x.shape[1])
             self._reduce(*dhs)
-        ops.segred_multi(meta, x, dhs, [bank.region_flat(bank.G, layer, nm, "A") for nm in names])  # K5
+        self._k5(lambda: ops.segred_multi(meta, x, dhs, [bank.region_flat(bank.G, layer, nm, "A") for nm in names]),
+                 x, *dhs)                                                                           # K5
         return dx
 
     def _token_major(self, x: torch.Tensor) -> torch.Tensor:
@@ -726,6 +748,9 @@ class PackedLoraTrainer:
             sv = saves.pop()
             dh = self._layer_bwd(layer, sv, dh, need_dx=layer > 0)
             del sv
+        if self._k5_used:   # the side stream's dA reductions before anything reads the grads
+            torch.cuda.current_stream().wait_stream(self._k5_stream)
+            self._k5_used = False
         return self.losses
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:

@@ -159,3 +159,30 @@ def test_dual_multi_target_one_launch(ks):
         assert not torch.isnan(dh).any() and not torch.isnan(g).any()
         assert rel(g, g_sep) < 1e-5, k
         assert rel(dh, dh_sep) < 2e-3, k
+
+
+def test_trainer_overlap_k5_identical_eager_and_graph():
+    """dA reductions on the side stream (overlap_k5): the same kernels on the same data,
+    so losses and every gradient are bit-identical to stream order, eager and replayed
+    from a CUDA graph (the side stream joins before the optimizer)."""
+    from paper_2508_02932_b200.model import PRESETS, PackedLoraTrainer, bench_adapters
+
+    specs, s = bench_adapters("tiny")
+    res = []
+    for overlap in (False, True):
+        tr = PackedLoraTrainer(PRESETS["tiny"], specs, s, device="cuda", a_scale=0.05, b_std=0.05,
+                               overlap_k5=overlap)
+        tokens = tr.synthetic_tokens().cuda()
+        losses = tr.forward_backward(tokens).float().clone()
+        res.append((losses, tr.bank.G.clone()))
+        if overlap:
+            g = tr.graphed(tokens, warmup=1)
+            g.graph.replay()
+            torch.cuda.synchronize()
+            tr2 = PackedLoraTrainer(PRESETS["tiny"], specs, s, device="cuda", a_scale=0.05, b_std=0.05)
+            tr2.step(tokens)          # same warm-up step as the graphed trainer's
+            l2 = tr2.forward_backward(tokens).float().clone()
+            assert torch.equal(g.losses.float(), l2)
+            assert torch.equal(tr.bank.G, tr2.bank.G)
+    assert torch.equal(res[0][0], res[1][0])
+    assert torch.equal(res[0][1], res[1][1])

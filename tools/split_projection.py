@@ -24,12 +24,15 @@ from paper_2508_02932_b200.sweep.engine import _base  # noqa: E402
 from paper_2508_02932_b200.sweep.jobsplit import split_adapters  # noqa: E402
 
 
+TRAINER_KW = {}
+
+
 def time_job(cfg_name, idx, steps, warmup, kernels=False, graph=False):
     cfg = PRESETS[cfg_name]
     specs, s = bench_adapters(cfg_name)
     sub = [specs[i] for i in idx]
     tr = PackedLoraTrainer(cfg, sub, s, device="cuda", base=_base(cfg_name, "cuda:0"),
-                           adapter_seeds=[100 + i for i in idx])
+                           adapter_seeds=[100 + i for i in idx], **TRAINER_KW)
     tok = tr.synthetic_tokens(seeds=[1000 + i for i in idx]).cuda()
     for _ in range(warmup):
         tr.step(tok)
@@ -79,10 +82,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--kernels", action="store_true", help="print each job's per-kernel-class times")
+    ap.add_argument("--overlap-k5", action="store_true", help="trainer option overlap_k5 (A/B)")
     ap.add_argument("--graph", action="store_true", help="time the step replayed from a CUDA graph")
     ap.add_argument("--whole-lora", action="store_true",
                     help="A/B: LoRA kernels without the pack workspace (whole tiles, no stream-K)")
     args = ap.parse_args()
+    if args.overlap_k5:
+        TRAINER_KW["overlap_k5"] = True
     if args.whole_lora:
         from paper_2508_02932_b200 import ops
 
