@@ -415,7 +415,7 @@ def main() -> None:
     if specs:
         trainer = PackedLoraTrainer(cfg, specs, s, device="cuda", adapter_seeds=[100 + i + seed_off for i in mine],
                                     tp=comm, fuse_dual=not args.no_fuse_dual,
-                                    overlap_k5=args.overlap_k5)
+                                    overlap_k5=True if args.overlap_k5 else None)
         T = trainer.T
         tokens_host = trainer.synthetic_tokens(seeds=[1000 + i + 100 * seed_off for i in mine]).pin_memory()
         tokens = tokens_host.to("cuda")

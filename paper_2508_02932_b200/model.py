@@ -212,7 +212,7 @@ class PackedLoraTrainer:
                  a_scale: float | None = None, b_std: float | Sequence[float] = 0.02, tp: Comm | None = None,
                  save_normed: bool | None = None, sequence_parallel: bool = True, tp_fused: bool = False,
                  tp_chunks: int = 4, fuse_swiglu: bool = True, fuse_dual: bool = True,
-                 fuse_swiglu_bwd: bool = True, overlap_k5: bool = False):
+                 fuse_swiglu_bwd: bool = True, overlap_k5: bool | None = None):
         """``tp``: a communicator over this job's tensor-parallel group (tp.py).  With
         tp.world > 1 every weight and adapter factor is this rank's Megatron shard and
         the step inserts the collectives described in tp.py; ``sequence_parallel`` (used
@@ -226,7 +226,9 @@ class PackedLoraTrainer:
         ``fuse_swiglu_bwd``: the SwiGLU backward and the down projection's dA in one kernel
         (ops.swiglu_bwd_segred: the activation never goes to HBM); ``overlap_k5``: the dA
         segment reductions (K5, off the critical path: only the optimizer reads dA) run on a
-        side stream beside the input-gradient GEMMs."""
+        side stream beside the input-gradient GEMMs (None: when the rank's step is small,
+        T <= 8192, where it fills the GEMMs' partial last waves -- +1.2% at the 8-GPU split's
+        T = 4096, neutral at T = 32768, profiles/r2_overlap_k5_ab.log)."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -277,6 +279,8 @@ class PackedLoraTrainer:
         self._fuse_swiglu = self.targets[4].h_out >= 256 and fuse_swiglu
         self._fuse_dual = bool(fuse_dual)
         self._fuse_swiglu_bwd = bool(fuse_swiglu_bwd)
+        if overlap_k5 is None:
+            overlap_k5 = self.T <= 8192
         self._overlap_k5 = bool(overlap_k5) and self.tp is None
         self._k5_stream = None
         self._k5_used = False
