@@ -50,16 +50,21 @@ class NullComm(Comm):
         return t
 
 
-def time_shard(cfg, specs, s, tp, steps, warmup):
-    tr = PackedLoraTrainer(cfg, specs, s, device="cuda", tp=NullComm(0, tp))
+TRAINER_KW = {}
+
+
+def time_shard(cfg, specs, s, tp, steps, warmup, graph=True):
+    tr = PackedLoraTrainer(cfg, specs, s, device="cuda", tp=NullComm(0, tp), **TRAINER_KW)
     tokens = tr.synthetic_tokens().cuda()
     for _ in range(warmup):
         tr.step(tokens)
     torch.cuda.synchronize()
+    run = tr.graphed(tokens, warmup=1).step if graph else (lambda: tr.step(tokens))   # as bench.py
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        tr.step(tokens)
+        run()
     e1.record()
     torch.cuda.synchronize()
     out = (e0.elapsed_time(e1) / steps, tr.T, torch.cuda.max_memory_allocated() / 1e9, tr.save_normed)
@@ -75,16 +80,28 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--depths", default="32,64")
+    ap.add_argument("--eager", action="store_true", help="time the eager step (default: the CUDA-graph step)")
+    ap.add_argument("--no-fuse-dual", action="store_true")
+    ap.add_argument("--no-fuse-swiglu-bwd", action="store_true")
     args = ap.parse_args()
+    if args.no_fuse_dual:
+        TRAINER_KW["fuse_dual"] = False
+    if args.no_fuse_swiglu_bwd:
+        TRAINER_KW["fuse_swiglu_bwd"] = False
     full = PRESETS["qwen2.5-32b"]
     specs, s = bench_adapters("qwen2.5-32b")
     depths = [int(x) for x in args.depths.split(",")]
     meas = {}
     for L in depths:
-        meas[L] = time_shard(dataclasses.replace(full, n_layers=L), specs, s, args.tp, args.steps, args.warmup)
-    (l0, (m0, T, mem0, sn0)), (l1, (m1, _, mem1, sn1)) = sorted(meas.items())[:2]
-    per_layer = (m1 - m0) / (l1 - l0)
-    ms = m0 + per_layer * (full.n_layers - l0)
+        meas[L] = time_shard(dataclasses.replace(full, n_layers=L), specs, s, args.tp, args.steps, args.warmup,
+                             graph=not args.eager)
+    if full.n_layers in meas:   # the full depth was measured: use it
+        ms, T = meas[full.n_layers][0], meas[full.n_layers][1]
+        per_layer = ms / full.n_layers
+    else:                       # extrapolate from two depths (every layer is identical work)
+        (l0, (m0, T, mem0, sn0)), (l1, (m1, _, mem1, sn1)) = sorted(meas.items())[:2]
+        per_layer = (m1 - m0) / (l1 - l0)
+        ms = m0 + per_layer * (full.n_layers - l0)
     cfg = full
     per_gpu_flops = cfg.base_flops_per_token() * T / args.tp
     ar_bytes = 4 * T * cfg.d * 2 * cfg.n_layers     # o + down fwd, qkv + gate/up bwd input grads (bf16)
@@ -100,6 +117,8 @@ def main():
         "measured": {str(L): {"ms_per_step": round(v[0], 1), "mem_peak_gb": round(v[2], 1), "save_normed": v[3]}
                      for L, v in meas.items()},
         "ms_per_layer": round(per_layer, 2),
+        "step_mode": "eager" if args.eager else "cuda_graph",
+        "trainer_options": TRAINER_KW,
     }), flush=True)
 
 
