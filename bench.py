@@ -354,6 +354,10 @@ def main() -> None:
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         raise SystemExit(_relaunch(args))
+    if args.config == "qwen2.5-32b":
+        # the 64-layer TP shard peaks at ~154 GB eagerly; a captured graph's private pool does
+        # not fit beside it (profiles/r2_c4_shard_projection.log): C4 times the eager step
+        args.graph = False
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
