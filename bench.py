@@ -614,6 +614,7 @@ def main() -> None:
         "roofline": {"bound": "tensor", "kernel": "tcgen05 base GEMM + fused LoRA expand (K1/K2b/K6, lm_head)",
                      "achieved": round(achieved, 1), "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
                      "frac": round(achieved / peaks["tflops_sustained"], 4), "traffic": _traffic(),
+                     "traffic_by_shape": _dram_by_shape() if args.config == "llama-3.1-8b" else None,
                      "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside a long step)",
                      "step_base_gemm_tflops": round(base_tf, 1),
                      "step_frac_of_burst_peak": round(base_tf / peaks["tflops_burst"], 4)},
@@ -670,6 +671,18 @@ def _traffic():
         return None
     try:
         return json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _dram_by_shape():
+    """DRAM bytes over algorithmic bytes per launch shape of one timed C3 step, from its
+    committed ncu launch list (profiles/r2_c3_step_dram_by_shape.json, tools/dram_by_shape.py)."""
+    prof = ROOT / "profiles" / "r2_c3_step_dram_by_shape.json"
+    try:
+        d = json.loads(prof.read_text())
+        return {"source": "profiles/r2_c3_step_dram_by_shape.json (ncu, one timed C3 step)",
+                "dram_over_algo": {k: v["dram_over_algo"] for k, v in d.items()}}
     except Exception:
         return None
 
