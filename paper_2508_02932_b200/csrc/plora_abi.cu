@@ -285,6 +285,9 @@ static constexpr int g_pair_nb_min_n = PLORA_PAIR512_MIN_N;
 // DRAM reads per GEMM -27%, SM clock under the power cap +45 MHz, +2.6% tokens/s vs
 // 8-row-group M-bands (the previous raster, PLORA_PAIR_BAND >= 0).
 static constexpr int g_pair_band = PLORA_PAIR_BAND;
+#ifndef PLORA_SWIGLU_BAND
+#define PLORA_SWIGLU_BAND PLORA_PAIR_BAND   // raster of the gate/up + SwiGLU launch (experiment knob)
+#endif
 
 // One segment of a (segmented) pair GEMM; see PairArgs in gemm_sm100.cuh.
 struct PairSeg {
@@ -390,7 +393,7 @@ static int run_pair_segments(cudaStream_t st, const plora_pack_t* pack, int64_t 
                                    cudaMemcpyDeviceToDevice, st));
     a.accumulate = 1;
   }
-  pa.band = g_pair_band;
+  pa.band = paired ? PLORA_SWIGLU_BAND : g_pair_band;
   if (paired) return launch_pair<false, 2, EPI_SWIGLU>(pa, st);
   if (NB == 2) return w_kmajor ? launch_pair<false, 2>(pa, st) : launch_pair<true, 2>(pa, st);
   return w_kmajor ? launch_pair<false, 1>(pa, st) : launch_pair<true, 1>(pa, st);
