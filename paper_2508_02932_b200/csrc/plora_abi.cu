@@ -709,11 +709,20 @@ static int run_swiglu_segred(cudaStream_t st, const plora_pack_t* pack, int64_t 
   a.M = static_cast<int>(ffn);
   a.mt_per = static_cast<int>((ffn + kBM - 1) / kBM);
   a.n_groups = pack->n_adapters * a.mt_per;
-  SegSched sched;
-  if (!segred_schedule(pack, a.mt_per, 1, &sched)) return fail("swiglu_bwd_segred: no tile schedule (host row offsets missing or too many tiles)");
+  // LPT tile schedule when the host row offsets are known and the tile count fits the
+  // schedule; otherwise round-robin tiles (sched.n_ctas = 0)
+  auto sched = std::make_unique<SegSched>();
+  int grid;
+  if (pack->h_row_off != nullptr && segred_schedule(pack, a.mt_per, 1, sched.get())) {
+    grid = sched->n_ctas;
+  } else {
+    memset(sched.get(), 0, sizeof(SegSched));
+    grid = a.n_groups < num_sms() ? a.n_groups : num_sms();
+  }
+  if (grid <= 0) return 0;
   static std::atomic<uint64_t> configured{0};
   if (ensure_smem(plora_swiglu_segred_kernel, kSwSmemBytes, configured)) return 1;
-  PLORA_CUDA(launch_pdl(plora_swiglu_segred_kernel, dim3(sched.n_ctas), dim3(kSwThreads), kSwSmemBytes, st, a, sched));
+  PLORA_CUDA(launch_pdl(plora_swiglu_segred_kernel, dim3(grid), dim3(kSwThreads), kSwSmemBytes, st, a, *sched));
   return 0;
 }
 

@@ -15,8 +15,9 @@
 // fp32 formulas on the bf16 inputs, bf16 rounding) and the MMA order that of the segment
 // reduction, so dg, du and dA are bit-identical to the two-kernel path.
 //
-// Roles (192 threads, 1 CTA/SM): warp 0 TMA producer, warp 1 MMA issuer, warps 2..5
-// transform + epilogue.  Tiles come from the same host LPT schedule as K3/K5 (SegSched).
+// Roles (1 CTA/SM): warp 0 TMA producer, warp 1 MMA issuer, 16 transform warps (the first
+// four also drain the accumulator).  Tiles come from the same host LPT schedule as K3/K5
+// (SegSched), or round-robin when the pack has no host row offsets (sched.n_ctas == 0).
 #pragma once
 #include "gemm_sm100.cuh"
 
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (TileIter it(&sched, 0); it.valid(); it.next()) {
+      for (TileIter it(sched.n_ctas ? &sched : nullptr, args.n_groups); it.valid(); it.next()) {
         const TileInfo t = sw_decode(args, it.tile());
         for (int b = 0; b < t.n_main; ++b) {
           mbar_wait(&empty[st], ph ^ 1);
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     constexpr uint32_t idesc = idesc_bf16(kBM, 64, true, true);
     int st = 0, acc = 0;
     uint32_t ph = 0, acc_phase = 0;
-    for (TileIter it(&sched, 0); it.valid(); it.next()) {
+    for (TileIter it(sched.n_ctas ? &sched : nullptr, args.n_groups); it.valid(); it.next()) {
       const TileInfo t = sw_decode(args, it.tile());
       if (t.n_main == 0) continue;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const int row = quarter * 32 + lane;
     int st = 0, acc = 0, pend = -1;     // pend: stage whose TMA stores are still reading smem
     uint32_t ph = 0, acc_phase = 0;
-    for (TileIter it(&sched, 0); it.valid(); it.next()) {
+    for (TileIter it(sched.n_ctas ? &sched : nullptr, args.n_groups); it.valid(); it.next()) {
       const TileInfo t = sw_decode(args, it.tile());
       const int ld = args.rpad_off[t.adapter + 1] - args.rpad_off[t.adapter];
       for (int b = 0; b < t.n_main; ++b) {

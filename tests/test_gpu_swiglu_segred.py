@@ -95,3 +95,20 @@ def test_trainer_fused_swiglu_bwd_matches():
         res.append((losses, tr.bank.G.clone()))
     assert torch.equal(res[0][0], res[1][0])
     assert torch.equal(res[0][1], res[1][1])
+
+
+def test_round_robin_tiles_without_host_offsets():
+    """A pack without host row offsets (plora_pack_t.h_row_off = NULL) runs the tiles
+    round-robin instead of the LPT schedule: same tiles, same MMA order, bit-identical."""
+    meta, da, g, u, dh = _operands(*CASES[1][1:3], 1792, seed=9)
+    ga = torch.empty(1792 * meta.rpad16_total, device="cuda")
+    dg, du = ops.swiglu_bwd_segred(meta, da, g, u, dh, ga)
+    saved = meta.struct.h_row_off
+    meta.struct.h_row_off = None
+    try:
+        ga2 = torch.full_like(ga, float("nan"))
+        dg2, du2 = ops.swiglu_bwd_segred(meta, da, g, u, dh, ga2)
+    finally:
+        meta.struct.h_row_off = saved
+    torch.cuda.synchronize()
+    assert torch.equal(dg, dg2) and torch.equal(du, du2) and torch.equal(ga, ga2)

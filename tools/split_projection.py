@@ -83,12 +83,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--kernels", action="store_true", help="print each job's per-kernel-class times")
     ap.add_argument("--overlap-k5", action="store_true", help="trainer option overlap_k5 (A/B)")
+    ap.add_argument("--no-overlap-k5", action="store_true", help="trainer option overlap_k5=False (A/B)")
     ap.add_argument("--graph", action="store_true", help="time the step replayed from a CUDA graph")
     ap.add_argument("--whole-lora", action="store_true",
                     help="A/B: LoRA kernels without the pack workspace (whole tiles, no stream-K)")
     args = ap.parse_args()
     if args.overlap_k5:
         TRAINER_KW["overlap_k5"] = True
+    if args.no_overlap_k5:
+        TRAINER_KW["overlap_k5"] = False
     if args.whole_lora:
         from paper_2508_02932_b200 import ops
 
