@@ -226,9 +226,8 @@ class PackedLoraTrainer:
         ``fuse_swiglu_bwd``: the SwiGLU backward and the down projection's dA in one kernel
         (ops.swiglu_bwd_segred: the activation never goes to HBM); ``overlap_k5``: the dA
         segment reductions (K5, off the critical path: only the optimizer reads dA) run on a
-        side stream beside the input-gradient GEMMs (None: when the rank's step is small,
-        T <= 8192, where it fills the GEMMs' partial last waves -- +1.2% at the 8-GPU split's
-        T = 4096, neutral at T = 32768, profiles/r2_overlap_k5_ab.log)."""
+        side stream beside the input-gradient GEMMs (None = off: within noise at T = 32768,
+        4096 and 8192 per rank, profiles/r2_overlap_k5_ab.log)."""
         self.cfg = cfg
         self.tp = tp if (tp is not None and tp.world > 1) else None
         self.shard = TPShard(tp.rank, tp.world) if self.tp is not None else TPShard()
@@ -280,7 +279,7 @@ class PackedLoraTrainer:
         self._fuse_dual = bool(fuse_dual)
         self._fuse_swiglu_bwd = bool(fuse_swiglu_bwd)
         if overlap_k5 is None:
-            overlap_k5 = self.T <= 8192
+            overlap_k5 = False
         self._overlap_k5 = bool(overlap_k5) and self.tp is None
         self._k5_stream = None
         self._k5_used = False
