@@ -754,13 +754,16 @@ struct DualPlan {
   int64_t part_h_floats;
 };
 
-// Best (rows per chunk, column chunks) of one target by the time model; 0 = the separate
-// kernels are expected to be faster.
-static void dual_choose(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, int* rcs_out, int* nc_out) {
-  *rcs_out = 0;
-  *nc_out = 0;
+// The (rows per chunk, column chunks) options of one target: units, cost of one unit and
+// fp32 partial bytes under the time model.
+struct DualOpt {
+  int rcs, nc;
+  int64_t units;
+  double unit_us, part_bytes;
+};
+
+static int dual_options(const plora_pack_t* pack, int64_t k, const int32_t* h_rpad_off, DualOpt* opt) {
   const int n = pack->n_adapters;
-  const int sms = num_sms();
   const int64_t T = pack->total_tokens;
   int64_t sum_rp = 0, tiles_all = 0;
   for (int a = 0; a < n; ++a) {
@@ -768,9 +771,9 @@ static void dual_choose(const plora_pack_t* pack, int64_t k, const int32_t* h_rp
     sum_rp += (h_rpad_off[a + 1] - h_rpad_off[a]) * tiles;   // partials scale with rpad16 per m-tile
     tiles_all += tiles;
   }
-  if (tiles_all == 0) return;
+  if (tiles_all == 0) return 0;
   const double avg_rp = static_cast<double>(sum_rp) / tiles_all;
-  double best_us = 2.0 * PLORA_DUAL_LAUNCH_US + 4.0 * T * k / (PLORA_DUAL_HBM_GBS * 1e3);   // separate K4 + K3
+  int no = 0;
   for (int rcs : {4, 2, 1}) {
     int64_t chunks = 0;
     for (int a = 0; a < n; ++a) {
@@ -781,22 +784,84 @@ static void dual_choose(const plora_pack_t* pack, int64_t k, const int32_t* h_rp
       const int64_t units = chunks * nc;
       if (units > kDualMaxUnits) break;
       const int64_t kc = ((k + nc - 1) / nc + 127) / 128 * 128;
-      const int64_t waves = (units + sms - 1) / sms;
-      const double unit_us = rcs * 128.0 * kc * 2 / (PLORA_DUAL_SM_GBS * 1e3) + PLORA_DUAL_UNIT_US;
-      const double part_bytes = 4.0 * avg_rp * (static_cast<double>(chunks) * k + (nc > 1 ? nc * static_cast<double>(T) : 0.0));
-      const double us = waves * unit_us + 2.0 * part_bytes / (PLORA_DUAL_HBM_GBS * 1e3) + PLORA_DUAL_LAUNCH_US;
-      if (us < best_us) {
-        best_us = us;
-        *rcs_out = rcs;
-        *nc_out = nc;
-      }
+      DualOpt& o = opt[no++];
+      o.rcs = rcs;
+      o.nc = nc;
+      o.units = units;
+      o.unit_us = rcs * 128.0 * kc * 2 / (PLORA_DUAL_SM_GBS * 1e3) + PLORA_DUAL_UNIT_US;
+      o.part_bytes = 4.0 * avg_rp * (static_cast<double>(chunks) * k + (nc > 1 ? nc * static_cast<double>(T) : 0.0));
     }
   }
+  return no;
 }
 
-// Plan of one fused launch over n_t targets of the pack (dY widths ks[t]) -- every target
-// gets its own (rows per chunk, column chunks) from dual_choose; the units of all targets
-// go into one unit list.  Returns the workspace bytes, or -1 when a target would be faster
+// Best options of the n_t targets of ONE launch, chosen jointly: the kernel hands unit u
+// to CTA u mod grid with the targets' units in sequence, so the main-loop time is the
+// heaviest CTA's sum of unit costs over all targets (a per-target choice would size each
+// target for the whole machine and the launch would run ~2 waves).  Compared against the
+// separate K4 + K3 passes of every target; false = those are expected to be faster.
+static bool dual_choose(const plora_pack_t* pack, int n_t, const int64_t* ks, const int32_t* h_rpad_off,
+                        int* rcs_out, int* nc_out) {
+  constexpr int kMaxOpt = 12;
+  DualOpt opt[kDualMaxTargets][kMaxOpt];
+  int no[kDualMaxTargets];
+  const int sms = num_sms();
+  const int64_t T = pack->total_tokens;
+  double sep_us = 0;
+  for (int t = 0; t < n_t; ++t) {
+    no[t] = dual_options(pack, ks[t], h_rpad_off, opt[t]);
+    if (no[t] == 0) return false;
+    sep_us += 2.0 * PLORA_DUAL_LAUNCH_US + 4.0 * T * ks[t] / (PLORA_DUAL_HBM_GBS * 1e3);
+  }
+  double best_us = sep_us;
+  bool found = false;
+  int idx[kDualMaxTargets] = {0, 0, 0};
+  for (;;) {
+    int64_t units = 0;
+    double work = 0, part = 0, cmax = 0;
+    for (int t = 0; t < n_t; ++t) {
+      const DualOpt& o = opt[t][idx[t]];
+      units += o.units;
+      work += o.units * o.unit_us;
+      part += o.part_bytes;
+      cmax = o.unit_us > cmax ? o.unit_us : cmax;
+    }
+    const double fixed = 2.0 * part / (PLORA_DUAL_HBM_GBS * 1e3) + PLORA_DUAL_LAUNCH_US;
+    const int64_t grid = units < sms ? units : sms;
+    const double lower = (work / grid > cmax ? work / grid : cmax) + fixed;
+    if (units <= kDualMaxUnits && lower < best_us) {
+      double tmain = 0;   // heaviest CTA: units [s, s + U_t) of target t, unit u on CTA u % grid
+      for (int64_t i = 0; i < grid; ++i) {
+        double load = 0;
+        int64_t s = 0;
+        for (int t = 0; t < n_t; ++t) {
+          const int64_t U = opt[t][idx[t]].units;
+          const int64_t cnt = (s + U - 1 - i >= 0 ? (s + U - 1 - i) / grid + 1 : 0) - (s - 1 - i >= 0 ? (s - 1 - i) / grid + 1 : 0);
+          load += cnt * opt[t][idx[t]].unit_us;
+          s += U;
+        }
+        tmain = load > tmain ? load : tmain;
+      }
+      const double us = tmain + fixed;
+      if (us < best_us) {
+        best_us = us;
+        found = true;
+        for (int t = 0; t < n_t; ++t) {
+          rcs_out[t] = opt[t][idx[t]].rcs;
+          nc_out[t] = opt[t][idx[t]].nc;
+        }
+      }
+    }
+    int t = 0;   // next combination
+    while (t < n_t && ++idx[t] == no[t]) idx[t++] = 0;
+    if (t == n_t) break;
+  }
+  return found;
+}
+
+// Plan of one fused launch over n_t targets of the pack (dY widths ks[t]) -- the targets'
+// (rows per chunk, column chunks) are chosen jointly by dual_choose; the units of all
+// targets go into one unit list.  Returns the workspace bytes, or -1 when a target would be faster
 // with the separate kernels or the pack is not eligible (rank blocks > 1, k % 128 != 0,
 // unit list or adapter table too large): then every target runs separately.
 static int64_t dual_plan(const plora_pack_t* pack, int n_t, const int64_t* ks, const int32_t* h_rpad_off,
@@ -814,19 +879,18 @@ static int64_t dual_plan(const plora_pack_t* pack, int n_t, const int64_t* ks, c
   f.n = n;
   int u = 0;
   int64_t boff = 0;   // floats
-  int rcs_t[kDualMaxTargets];
+  int rcs_t[kDualMaxTargets], nc_t[kDualMaxTargets];
+  for (int t = 0; t < n_t; ++t)
+    if (ks[t] <= 0 || ks[t] % 128 || ks[t] > (1 << 24)) return -1;
+  if (!dual_choose(pack, n_t, ks, h_rpad_off, rcs_t, nc_t)) return -1;
   for (int t = 0; t < n_t; ++t) {
     const int64_t k = ks[t];
-    if (k <= 0 || k % 128 || k > (1 << 24)) return -1;
-    int rcs, nc;
-    dual_choose(pack, k, h_rpad_off, &rcs, &nc);
-    if (rcs == 0) return -1;
+    int nc = nc_t[t];
     const int kc = static_cast<int>(((k + nc - 1) / nc + 127) / 128 * 128);
     nc = static_cast<int>((k + kc - 1) / kc);
     sc.tg[t].k = static_cast<int>(k);
     sc.tg[t].kc = kc;
     sc.tg[t].nc = nc;
-    rcs_t[t] = rcs;
   }
   for (int t = 0; t < n_t; ++t) {
     const int rcs = rcs_t[t], nc = sc.tg[t].nc, kc = sc.tg[t].kc;
