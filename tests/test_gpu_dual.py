@@ -131,16 +131,21 @@ def test_trainer_fused_dual_matches_separate():
     assert rel(res[0][1], res[1][1]) < 5e-3
 
 
+PACKS = {"c3": (C3_RANKS, C3_TOKENS), "split8-1": ([64], [4096]), "split8-3": ([8, 32, 32], [1024, 2048, 1024])}
+
+
+@pytest.mark.parametrize("pack", list(PACKS))
 @pytest.mark.parametrize("ks", [(4096, 1024, 1024), (14336, 14336)])
-def test_dual_multi_target_one_launch(ks):
+def test_dual_multi_target_one_launch(ks, pack):
     """The q/k/v (or gate/up) targets of a layer in ONE fused launch equal the separate
-    K4 / K3 kernels per target (fp32 association)."""
+    K4 / K3 kernels per target (fp32 association) -- on C3 and on planner-split rank packs,
+    whose jointly planned launches mix targets of different unit sizes."""
     import ctypes
-    outs, refs = [], []
+    ranks, tokens = PACKS[pack]
     meta = None
     dys, bts, hss = [], [], []
     for j, k in enumerate(ks):
-        m, dy, bt, hs = _operands(C3_RANKS, C3_TOKENS, k, seed=20 + j)
+        m, dy, bt, hs = _operands(ranks, tokens, k, seed=20 + j)
         meta = meta or m
         dys.append(dy), bts.append(bt), hss.append(hs)
     T, R64 = meta.total_tokens, meta.rpad64
