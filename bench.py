@@ -614,7 +614,7 @@ def main() -> None:
         "roofline": {"bound": "tensor", "kernel": "tcgen05 base GEMM + fused LoRA expand (K1/K2b/K6, lm_head)",
                      "achieved": round(achieved, 1), "peak": peaks["tflops_sustained"], "unit": "TFLOP/s",
                      "frac": round(achieved / peaks["tflops_sustained"], 4), "traffic": _traffic(),
-                     "traffic_by_shape": _dram_by_shape() if args.config == "llama-3.1-8b" else None,
+                     "traffic_by_shape": _dram_by_shape(peaks["hbm_gbs"]) if args.config == "llama-3.1-8b" else None,
                      "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside a long step)",
                      "step_base_gemm_tflops": round(base_tf, 1),
                      "step_frac_of_burst_peak": round(base_tf / peaks["tflops_burst"], 4)},
@@ -675,14 +675,19 @@ def _traffic():
         return None
 
 
-def _dram_by_shape():
+def _dram_by_shape(hbm_peak_gbs: float):
     """DRAM bytes over algorithmic bytes per launch shape of one timed C3 step, from its
-    committed ncu launch list (profiles/r2_c3_step_dram_by_shape.json, tools/dram_by_shape.py)."""
+    committed ncu launch list (profiles/r2_c3_step_dram_by_shape.json, tools/dram_by_shape.py),
+    and for the HBM-bound LoRA / optimizer shapes the algorithmic bytes over ncu's launch
+    duration (serialised, no launch gap) as a fraction of the HBM peak -- beside the in-graph
+    event timing of `kernels`, which includes each launch's ramp-up and gap."""
     prof = ROOT / "profiles" / "r2_c3_step_dram_by_shape.json"
     try:
         d = json.loads(prof.read_text())
         return {"source": "profiles/r2_c3_step_dram_by_shape.json (ncu, one timed C3 step)",
-                "dram_over_algo": {k: v["dram_over_algo"] for k, v in d.items()}}
+                "dram_over_algo": {k: v["dram_over_algo"] for k, v in d.items()},
+                "hbm_frac_ncu": {k: round(v["algo_gb_per_launch"] / (v["ncu_ms_per_launch"] * 1e-3) / hbm_peak_gbs, 3)
+                                 for k, v in d.items() if not k.startswith("gemm")}}
     except Exception:
         return None
 
