@@ -861,8 +861,8 @@ static bool dual_choose(const plora_pack_t* pack, int n_t, const int64_t* ks, co
 
 // Plan of one fused launch over n_t targets of the pack (dY widths ks[t]) -- the targets'
 // (rows per chunk, column chunks) are chosen jointly by dual_choose; the units of all
-// targets go into one unit list.  Returns the workspace bytes, or -1 when a target would be faster
-// with the separate kernels or the pack is not eligible (rank blocks > 1, k % 128 != 0,
+// targets go into one unit list.  Returns the workspace bytes, or -1 when the separate
+// kernels are expected to be faster or the pack is not eligible (rank blocks > 1, k % 128 != 0,
 // unit list or adapter table too large): then every target runs separately.
 static int64_t dual_plan(const plora_pack_t* pack, int n_t, const int64_t* ks, const int32_t* h_rpad_off,
                          DualPlan* plan) {
